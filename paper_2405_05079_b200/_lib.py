@@ -1,0 +1,108 @@
+"""ctypes binding of libpovar.so (include/povar.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``).  There
+is no CPU fallback: if the shared library or a CUDA device is missing, every
+entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .types import NumericFailureError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpovar.so")
+
+PV_OK, PV_EINVAL, PV_ECUDA, PV_ENCCL, PV_ENONFINITE, PV_EDEGENERATE = range(6)
+PV_CURRENT, PV_TRIAL = 0, 1
+(PV_DBG_U, PV_DBG_UINV, PV_DBG_BP, PV_DBG_V, PV_DBG_VPINV, PV_DBG_BL, PV_DBG_DEGEN, PV_DBG_W,
+ PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN) = range(12)
+INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
+               "device_bytes", "n_l_global")
+PV_INFO_COUNT = 16
+
+# (name, restype, argtypes) of every exported symbol declared in include/povar.h
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.POINTER(ctypes.c_int64)
+SIGNATURES = [
+    ("pv_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("pv_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                 _I64, _I64, _D, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.c_double]),
+    ("pv_destroy", None, [_P]),
+    ("pv_last_error", ctypes.c_char_p, [_P]),
+    ("pv_info", ctypes.c_int, [_P, _I64]),
+    ("pv_stream", _P, [_P]),
+    ("pv_set_state", ctypes.c_int, [_P, _D, _D]),
+    ("pv_get_state", ctypes.c_int, [_P, _D, _D]),
+    ("pv_get_trial", ctypes.c_int, [_P, _D, _D]),
+    ("pv_cost", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _D]),
+    ("pv_linearize", ctypes.c_int, [_P, ctypes.c_int]),
+    ("pv_damp", ctypes.c_int, [_P, ctypes.c_double, ctypes.c_int, _I64]),
+    ("pv_power_solve", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double,
+                                      ctypes.POINTER(ctypes.c_int), _D]),
+    ("pv_trial", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    ("pv_accept", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _D, _I64]),
+    ("pv_resolve_current", ctypes.c_int, [_P, _I64]),
+    ("pv_get_step", ctypes.c_int, [_P, _D, _D]),
+    ("pv_schur_apply", ctypes.c_int, [_P, ctypes.c_int, _D, _D]),
+    ("pv_bench_terms", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_float)]),
+    ("pv_debug_get", ctypes.c_int, [_P, ctypes.c_int, _D]),
+]
+
+_lib = None
+
+
+class PovarLibraryError(RuntimeError):
+    """libpovar.so is missing or failed to load (no CPU fallback exists)."""
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise PovarLibraryError(
+            f"{LIB_PATH} not found: build it with `make` (or __graft_entry__.build()); "
+            "the PoVar path has no CPU fallback")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover - depends on the host
+        raise PovarLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error(ctx) -> str:
+    msg = load().pv_last_error(ctx)
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, ctx=None) -> None:
+    if rc == PV_OK:
+        return
+    msg = last_error(ctx)
+    if rc == PV_EINVAL:
+        raise ValueError(msg)
+    if rc == PV_ENONFINITE:
+        raise NumericFailureError(msg)
+    if rc == PV_EDEGENERATE:
+        raise FloatingPointError(msg)
+    kind = "NCCL" if rc == PV_ENCCL else "CUDA"
+    raise RuntimeError(f"libpovar {kind} error ({rc}): {msg}")
+
+
+def dptr(a):
+    return a.ctypes.data_as(_D)
+
+
+def i64ptr(a):
+    return a.ctypes.data_as(_I64)

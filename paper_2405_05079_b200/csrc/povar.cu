@@ -1,0 +1,951 @@
+// libpovar.so: device-resident context + C-ABI (include/povar.h).
+//
+// Host side of the B200 PoVar hot path: builds the landmark-CSR / camera-chunk
+// work decomposition once per problem, owns the device buffers, the CUDA
+// stream and (world > 1) the NCCL communicator, and sequences the kernels of
+// pv_kernels.cuh.  The LM state machine itself stays in Python
+// (paper_2405_05079_b200/solver.py, mirroring solvers.py:318-393).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/povar.h"
+#include "pv_kernels.cuh"
+
+using namespace pv;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct PvError : std::runtime_error {
+  int code;
+  PvError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw PvError(PV_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+#define NK(x)                                                                              \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess)                                                                 \
+      throw PvError(PV_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));            \
+  } while (0)
+
+inline int blocks_for(long long n, int per) { return (int)std::max(1LL, (n + per - 1) / per); }
+
+}  // namespace
+
+struct pv_ctx {
+  int device = 0, rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::string err;
+  long long launches = 0;
+  size_t device_bytes = 0;
+  std::vector<void*> allocs;
+
+  int64_t n_p = 0, n_l_global = 0, n_o_global = 0;
+  int n_ls = 0, n_os = 0, n_tasks = 0, n_chunks = 0;
+  std::vector<int64_t> lm_gid;  // local -> global landmark id
+  Coef coef{};
+
+  // graph (device)
+  Graph g{};
+  int *d_ls_cam = nullptr, *d_lm_off = nullptr, *d_task_lm = nullptr, *d_cs_lm = nullptr,
+      *d_chunk_off = nullptr, *d_chunk_cam = nullptr, *d_cam_chunk = nullptr;
+  double *d_ls_m = nullptr, *d_cs_m = nullptr;
+
+  // state and solve buffers (device)
+  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam;
+  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cyc, *cyr, *lin_part, *cUraw, *nrm, *cpart,
+      *ctmp, *scal;
+  int* flags;
+  unsigned* ticket;
+  PowerCtl* ctl;
+  PowerCtl* host_ctl = nullptr;  // mapped pinned mirror
+  PowerCtl* host_ctl_dev = nullptr;
+
+  int lin_stage = 0;
+  bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
+  int step_stage = 0;
+
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemsetAsync(p, 0, bytes, stream));
+    allocs.push_back(p);
+    device_bytes += bytes;
+    return static_cast<T*>(p);
+  }
+
+  void launched(int n = 1) { launches += n; }
+  void check_launch() { CK(cudaGetLastError()); }
+
+  void allreduce(double* p, size_t n) {
+    if (world > 1) NK(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, stream));
+  }
+  void allreduce_flags() {
+    if (world > 1) NK(ncclAllReduce(flags, flags, F_COUNT, ncclInt32, ncclMax, comm, stream));
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+
+  int nblk_tasks() const { return blocks_for((long long)n_tasks * 32, 256); }
+  int nblk_chunks() const { return blocks_for((long long)n_chunks * 32, 256); }
+  int nblk_epi() const { return blocks_for(n_p * 16, 256); }
+};
+
+// ---------------------------------------------------------------------------
+// graph construction (host, O(n) counting sorts)
+
+static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx,
+                        const double* meas, int64_t lm_begin, int64_t lm_end) {
+  const int64_t n_o = c->n_o_global, n_p = c->n_p;
+  const int64_t span = lm_end - lm_begin;
+  std::vector<int64_t> cnt(span, 0);
+  for (int64_t o = 0; o < n_o; ++o) {
+    int64_t l = lm_idx[o];
+    if (l >= lm_begin && l < lm_end) cnt[l - lm_begin]++;
+  }
+  std::vector<int> lid(span, -1);
+  c->lm_gid.clear();
+  for (int64_t j = 0; j < span; ++j)
+    if (cnt[j] > 0) {
+      lid[j] = (int)c->lm_gid.size();
+      c->lm_gid.push_back(lm_begin + j);
+    }
+  const int n_ls = (int)c->lm_gid.size();
+  int64_t n_os = 0;
+  for (int64_t j = 0; j < span; ++j) n_os += cnt[j];
+  if (n_os >= (int64_t)INT32_MAX) throw PvError(PV_EINVAL, "shard has too many observations");
+  c->n_ls = n_ls;
+  c->n_os = (int)n_os;
+
+  // stable counting sort by camera, then stable by local landmark
+  std::vector<int64_t> ccount(n_p + 1, 0);
+  for (int64_t o = 0; o < n_o; ++o) {
+    int64_t l = lm_idx[o];
+    if (l >= lm_begin && l < lm_end) ccount[cam_idx[o] + 1]++;
+  }
+  for (int64_t i = 0; i < n_p; ++i) ccount[i + 1] += ccount[i];
+  std::vector<int64_t> by_cam(n_os);
+  {
+    std::vector<int64_t> pos(ccount.begin(), ccount.end() - 1);
+    for (int64_t o = 0; o < n_o; ++o) {
+      int64_t l = lm_idx[o];
+      if (l >= lm_begin && l < lm_end) by_cam[pos[cam_idx[o]]++] = o;
+    }
+  }
+  std::vector<int> lm_off(n_ls + 1, 0);
+  for (int j = 0; j < n_ls; ++j) lm_off[j + 1] = lm_off[j] + (int)cnt[c->lm_gid[j] - lm_begin];
+  std::vector<int> ls_cam(n_os), ls_lid(n_os);
+  std::vector<double> ls_m(2 * n_os);
+  {
+    std::vector<int> pos(lm_off.begin(), lm_off.end() - 1);
+    for (int64_t k = 0; k < n_os; ++k) {
+      int64_t o = by_cam[k];
+      int l = lid[lm_idx[o] - lm_begin];
+      int p = pos[l]++;
+      ls_cam[p] = (int)cam_idx[o];
+      ls_lid[p] = l;
+      ls_m[2 * p] = meas[2 * o];
+      ls_m[2 * p + 1] = meas[2 * o + 1];
+    }
+  }
+  // camera-sorted permutation of the landmark-sorted rows
+  std::vector<int> cam_off(n_p + 1, 0);
+  for (int64_t k = 0; k < n_os; ++k) cam_off[ls_cam[k] + 1]++;
+  for (int64_t i = 0; i < n_p; ++i) cam_off[i + 1] += cam_off[i];
+  std::vector<int> cs_lm(n_os);
+  std::vector<double> cs_m(2 * n_os);
+  {
+    std::vector<int> pos(cam_off.begin(), cam_off.end() - 1);
+    for (int64_t k = 0; k < n_os; ++k) {
+      int p = pos[ls_cam[k]]++;
+      cs_lm[p] = ls_lid[k];
+      cs_m[2 * p] = ls_m[2 * k];
+      cs_m[2 * p + 1] = ls_m[2 * k + 1];
+    }
+  }
+  // camera chunks
+  std::vector<int> chunk_off, chunk_cam, cam_chunk(n_p + 1, 0);
+  for (int64_t i = 0; i < n_p; ++i) {
+    cam_chunk[i] = (int)chunk_cam.size();
+    for (int s = cam_off[i]; s < cam_off[i + 1]; s += PV_CHUNK) {
+      chunk_off.push_back(s);
+      chunk_cam.push_back((int)i);
+    }
+  }
+  cam_chunk[n_p] = (int)chunk_cam.size();
+  chunk_off.push_back((int)n_os);
+  // landmark tasks: whole landmarks packed into <= 32 lanes, or one long landmark
+  std::vector<int> task_lm;
+  {
+    int j = 0;
+    while (j < n_ls) {
+      task_lm.push_back(j);
+      int k = lm_off[j + 1] - lm_off[j];
+      if (k > 32) {
+        ++j;
+        continue;
+      }
+      int total = k, nl = 1;
+      ++j;
+      while (j < n_ls && nl < 32) {
+        int kk = lm_off[j + 1] - lm_off[j];
+        if (kk > 32 || total + kk > 32) break;
+        total += kk;
+        ++nl;
+        ++j;
+      }
+    }
+    task_lm.push_back(n_ls);
+  }
+  c->n_tasks = (int)task_lm.size() - 1;
+  c->n_chunks = (int)chunk_cam.size();
+
+  auto up_i = [&](const std::vector<int>& v) {
+    int* d = c->alloc<int>(v.size());
+    CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    return d;
+  };
+  auto up_d = [&](const std::vector<double>& v) {
+    double* d = c->alloc<double>(v.size());
+    CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    return d;
+  };
+  c->d_ls_cam = up_i(ls_cam);
+  c->d_ls_m = up_d(ls_m);
+  c->d_lm_off = up_i(lm_off);
+  c->d_task_lm = up_i(task_lm);
+  c->d_cs_lm = up_i(cs_lm);
+  c->d_cs_m = up_d(cs_m);
+  c->d_chunk_off = up_i(chunk_off);
+  c->d_chunk_cam = up_i(chunk_cam);
+  c->d_cam_chunk = up_i(cam_chunk);
+  c->sync();  // host vectors go out of scope
+
+  Graph& g = c->g;
+  g.n_p = (int)n_p;
+  g.n_l = n_ls;
+  g.n_o = (int)n_os;
+  g.n_tasks = c->n_tasks;
+  g.n_chunks = c->n_chunks;
+  g.ls_cam = c->d_ls_cam;
+  g.ls_m = c->d_ls_m;
+  g.lm_off = c->d_lm_off;
+  g.task_lm = c->d_task_lm;
+  g.cs_lm = c->d_cs_lm;
+  g.cs_m = c->d_cs_m;
+  g.chunk_off = c->d_chunk_off;
+  g.chunk_cam = c->d_chunk_cam;
+  g.cam_chunk = c->d_cam_chunk;
+}
+
+static void alloc_buffers(pv_ctx* c) {
+  const size_t np = c->n_p, nl = c->n_ls;
+  c->crec = c->alloc<double>(np * CREC);
+  c->lrec = c->alloc<double>(nl * LREC);
+  c->lsys = c->alloc<double>(nl * LSYS);
+  c->lvr = c->alloc<double>(nl * 8);
+  c->lbl = c->alloc<double>(nl * 4);
+  c->ldl = c->alloc<double>(nl * 4);
+  c->tlm = c->alloc<double>(nl * 4);
+  c->tcam = c->alloc<double>(np * 12);
+  c->cU = c->alloc<double>(np * 144);
+  c->cUd = c->alloc<double>(np * 144);
+  c->cUi = c->alloc<double>(np * 144);
+  c->cbp = c->alloc<double>(np * 12);
+  c->cx = c->alloc<double>(np * 12);
+  c->crhs = c->alloc<double>(np * 12);
+  c->ch = c->alloc<double>(np * 12);
+  c->cyc = c->alloc<double>((size_t)c->n_chunks * 12);
+  c->cyr = c->alloc<double>(np * 12);
+  c->lin_part = c->alloc<double>((size_t)c->n_chunks * LINP);
+  c->cUraw = c->alloc<double>(np * LINP);
+  c->nrm = c->alloc<double>(np * 2);
+  c->cpart = c->alloc<double>((size_t)c->nblk_tasks());
+  c->ctmp = c->alloc<double>(np * 12);
+  c->scal = c->alloc<double>(8);
+  c->flags = c->alloc<int>(F_COUNT);
+  c->ticket = c->alloc<unsigned>(4);
+  c->ctl = c->alloc<PowerCtl>(1);
+  CK(cudaHostAlloc((void**)&c->host_ctl, sizeof(PowerCtl), cudaHostAllocMapped));
+  std::memset(c->host_ctl, 0, sizeof(PowerCtl));
+  CK(cudaHostGetDevicePointer((void**)&c->host_ctl_dev, c->host_ctl, 0));
+}
+
+// ---------------------------------------------------------------------------
+// operations
+
+template <int S>
+static void op_cost(pv_ctx* c, int which, double* f) {
+  const double* cams = which == PV_TRIAL ? c->tcam : c->crec;
+  const int cs = which == PV_TRIAL ? 12 : CREC;
+  const double* lms = which == PV_TRIAL ? c->tlm : c->lrec;
+  const int ls = which == PV_TRIAL ? 4 : LREC;
+  CK(cudaMemsetAsync(c->flags + F_INVALID_Z, 0, sizeof(int), c->stream));
+  const int nb = c->nblk_tasks();
+  k_cost<S><<<nb, 256, 0, c->stream>>>(c->g, cams, cs, lms, ls, c->cpart, c->flags, c->coef);
+  k_sum<<<1, 1024, 0, c->stream>>>(c->cpart, nb, c->scal);
+  c->launched(2);
+  c->check_launch();
+  c->allreduce(c->scal, 1);
+  c->allreduce_flags();
+  double v = 0.0;
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(&v, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  *f = (S == 2 && fl[F_INVALID_Z]) ? INFINITY : v;
+}
+
+template <int S>
+static int op_linearize(pv_ctx* c) {
+  CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
+  k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr, c->lbl,
+                                                      c->flags, c->coef);
+  k_lin_cam<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lin_part,
+                                                        c->coef);
+  k_lin_cam_reduce<<<blocks_for(c->n_p * LINP, 256), 256, 0, c->stream>>>(c->g, c->lin_part,
+                                                                         c->cUraw);
+  c->launched(3);
+  c->check_launch();
+  c->allreduce(c->cUraw, (size_t)c->n_p * LINP);
+  k_lin_cam_project<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>(
+      (int)c->n_p, c->cUraw, c->crec, c->cU, c->cbp, c->ch);
+  c->launched();
+  c->check_launch();
+  c->allreduce_flags();
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  c->lin_stage = S;
+  c->vp_cached = false;
+  if (S == 2 && fl[F_INVALID_Z]) {
+    c->lin_stage = 0;
+    return PV_EDEGENERATE;
+  }
+  return PV_OK;
+}
+
+template <int S>
+static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
+  const int D = S == 1 ? 12 : 11;
+  CK(cudaMemsetAsync(c->flags + F_SINGULAR_U, 0, 2 * sizeof(int), c->stream));
+  k_damp_cam<<<blocks_for(c->n_p, 64), 64, 0, c->stream>>>((int)c->n_p, D, c->cU, lam, c->cUd,
+                                                           c->cUi, c->flags);
+  c->launched();
+  if (both || !c->vp_cached) {
+    k_damp_lm<S><<<blocks_for(c->n_ls, 256), 256, 0, c->stream>>>(
+        c->n_ls, c->lvr, c->lbl, c->lrec, c->lsys, lam, both, c->flags);
+    c->launched();
+    c->vp_cached = !both;
+  }
+  c->check_launch();
+  c->allreduce_flags();
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (n_deg) *n_deg = fl[F_N_DEGEN];
+}
+
+template <int S>
+static void launch_epilogue(pv_ctx* c, int mode, int term, double thr) {
+  auto go = [&](int part) {
+    switch (mode) {
+      case EPI_RHS:
+        k_epilogue<S, EPI_RHS><<<c->nblk_epi(), 256, 0, c->stream>>>(
+            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
+            c->host_ctl_dev, c->ticket, part, term, thr);
+        break;
+      case EPI_TERM:
+        k_epilogue<S, EPI_TERM><<<c->nblk_epi(), 256, 0, c->stream>>>(
+            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
+            c->host_ctl_dev, c->ticket, part, term, thr);
+        break;
+      default:
+        k_epilogue<S, EPI_RAW><<<c->nblk_epi(), 256, 0, c->stream>>>(
+            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
+            c->host_ctl_dev, c->ticket, part, term, thr);
+    }
+    c->launched();
+  };
+  if (c->world > 1) {
+    go(EPI_REDUCE_ONLY);
+    c->allreduce(c->cyr, (size_t)c->n_p * 12);
+    go(EPI_APPLY_ONLY);
+  } else {
+    go(EPI_FULL);
+  }
+}
+
+template <int S>
+static void launch_term(pv_ctx* c, int term, double thr) {
+  k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
+      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
+  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 1,
+                                                       c->coef);
+  c->launched(2);
+  launch_epilogue<S>(c, EPI_TERM, term, thr);
+}
+
+template <int S>
+static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* trunc) {
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
+  CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
+  c->sync();
+  std::memset(c->host_ctl, 0, sizeof(PowerCtl));
+  // K4: reduced RHS and t_0 = U^-1 rhs
+  k_lm_rhs_t<S><<<blocks_for(c->n_ls, 256), 256, 0, c->stream>>>(c->n_ls, c->lbl, c->lsys,
+                                                                  c->lrec);
+  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 0,
+                                                       c->coef);
+  c->launched(2);
+  launch_epilogue<S>(c, EPI_RHS, 0, thr);
+  c->check_launch();
+  // K5 + K6 terms with a one-term lookahead on the device stop flag
+  for (int i = 1; i <= max_order; ++i) {
+    launch_term<S>(c, i, thr);
+    CK(cudaEventRecord(c->ev[i & 1], c->stream));
+    if (i >= 2) {
+      CK(cudaEventSynchronize(c->ev[(i - 1) & 1]));
+      if (((volatile PowerCtl*)c->host_ctl)->stopped) break;
+    }
+  }
+  c->check_launch();
+  // K7 back-substitution with v = x
+  k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
+  k_phase1<S, P1_BACKSUB><<<c->nblk_tasks(), 256, 0, c->stream>>>(
+      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
+  c->launched(2);
+  c->check_launch();
+  PowerCtl h;
+  CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  *order = h.order;
+  *trunc = h.trunc;
+  c->step_stage = S;
+}
+
+template <int S>
+static void op_trial(pv_ctx* c, int* ok) {
+  k_trial_cam<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->crec, c->cx,
+                                                                  c->ch, c->tcam, c->flags);
+  c->launched();
+  c->check_launch();
+  c->allreduce_flags();
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  *ok = fl[F_ZERO_NORM] ? 0 : 1;
+}
+
+static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
+  CK(cudaMemsetAsync(c->flags + F_N_RANKDEF, 0, sizeof(int), c->stream));
+  const int nb = c->nblk_tasks();
+  k_resolve<<<nb, 256, 0, c->stream>>>(c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef);
+  k_sum<<<1, 1024, 0, c->stream>>>(c->cpart, nb, c->scal);
+  c->launched(2);
+  c->check_launch();
+  c->allreduce(c->scal, 1);
+  c->allreduce_flags();
+  double v;
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(&v, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (f_new) *f_new = v;
+  if (n_rd) *n_rd = fl[F_N_RANKDEF];
+}
+
+static void op_accept(pv_ctx* c) {
+  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
+  k_accept<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, c->tcam, c->tlm,
+                                                      c->crec, c->lrec);
+  c->launched();
+  c->check_launch();
+  c->lin_stage = 0;
+  c->vp_cached = false;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+
+#define API_BEGIN(ctx) \
+  if (!(ctx)) return PV_EINVAL; \
+  try {
+#define API_END(ctx)                              \
+  }                                               \
+  catch (const PvError& e) {                      \
+    (ctx)->err = e.what();                        \
+    return e.code;                                \
+  }                                               \
+  catch (const std::exception& e) {               \
+    (ctx)->err = e.what();                        \
+    return PV_ECUDA;                              \
+  }                                               \
+  return PV_OK;
+
+#define STAGE_DISPATCH(stage, fn, ...)                                          \
+  ((stage) == 1 ? fn<1>(__VA_ARGS__)                                            \
+                : ((stage) == 2 ? fn<2>(__VA_ARGS__)                            \
+                                : throw PvError(PV_EINVAL, "stage must be 1 or 2")))
+
+extern "C" {
+
+int pv_nccl_unique_id(unsigned char out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PV_ENCCL;
+  static_assert(sizeof(id) == 128, "nccl id size");
+  std::memcpy(out, &id, 128);
+  return PV_OK;
+}
+
+int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char* nccl_id,
+              int64_t n_cameras, int64_t n_landmarks, int64_t n_obs, const int64_t* cam_idx,
+              const int64_t* lm_idx, const double* meas, int64_t lm_begin, int64_t lm_end,
+              double eta) {
+  g_create_error.clear();
+  if (!out) return PV_EINVAL;
+  *out = nullptr;
+  pv_ctx* c = new pv_ctx();
+  try {
+    if (n_cameras < 0 || n_landmarks < 0 || n_obs < 0 || world < 1 || rank < 0 ||
+        rank >= world || lm_begin < 0 || lm_end > n_landmarks || lm_begin > lm_end)
+      throw PvError(PV_EINVAL, "invalid sizes or shard range");
+    if (n_cameras >= INT32_MAX || n_landmarks >= INT32_MAX)
+      throw PvError(PV_EINVAL, "problem too large for int32 indexing");
+    if (!(eta >= 0.0 && eta <= 1.0)) throw PvError(PV_EINVAL, "eta must lie in [0, 1]");
+    if (n_obs > 0 && (!cam_idx || !lm_idx || !meas)) throw PvError(PV_EINVAL, "null arrays");
+    for (int64_t o = 0; o < n_obs; ++o) {
+      if (cam_idx[o] < 0 || cam_idx[o] >= n_cameras)
+        throw PvError(PV_EINVAL, "camera index out of range");
+      if (lm_idx[o] < 0 || lm_idx[o] >= n_landmarks)
+        throw PvError(PV_EINVAL, "landmark index out of range");
+    }
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    c->n_p = n_cameras;
+    c->n_l_global = n_landmarks;
+    c->n_o_global = n_obs;
+    c->coef.s1 = std::sqrt(1.0 - eta);
+    c->coef.s2 = std::sqrt(eta);
+    c->coef.s = 1.0 - eta;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->tev) CK(cudaEventCreate(&e));
+    if (world > 1) {
+      if (!nccl_id) throw PvError(PV_EINVAL, "nccl id required for world > 1");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&c->comm, world, id, rank));
+    }
+    // factor table of the camera linearization (record offsets, see k_lin_cam)
+    {
+      unsigned char tab[LINP][3];
+      const int symidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+      int e = 0;
+      for (int i = 0; i < 12; ++i)
+        for (int j = i; j < 12; ++j, ++e) {
+          tab[e][0] = (unsigned char)(4 + symidx[i / 4][j / 4]);
+          tab[e][1] = (unsigned char)(i % 4);
+          tab[e][2] = (unsigned char)(j % 4);
+        }
+      for (int kk = 0; kk < 12; ++kk, ++e) {
+        tab[e][0] = (unsigned char)(10 + kk / 4);
+        tab[e][1] = (unsigned char)(kk % 4);
+        tab[e][2] = 13;  // constant 1
+      }
+      CK(cudaMemcpyToSymbol(c_lin_idx, tab, sizeof(tab)));
+    }
+    build_graph(c, cam_idx, lm_idx, meas, lm_begin, lm_end);
+    alloc_buffers(c);
+    c->sync();
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    int code = PV_ECUDA;
+    if (auto pe = dynamic_cast<const PvError*>(&e)) code = pe->code;
+    pv_destroy(c);
+    return code;
+  }
+  *out = c;
+  return PV_OK;
+}
+
+void pv_destroy(pv_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->host_ctl) cudaFreeHost(c->host_ctl);
+  for (auto e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : c->tev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* pv_last_error(pv_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+void* pv_stream(pv_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int pv_info(pv_ctx* c, int64_t* out) {
+  API_BEGIN(c)
+  std::fill(out, out + PV_INFO_COUNT, 0);
+  out[PV_INFO_NP] = c->n_p;
+  out[PV_INFO_NL_LOCAL] = c->n_ls;
+  out[PV_INFO_NO_LOCAL] = c->n_os;
+  out[PV_INFO_TASKS] = c->n_tasks;
+  out[PV_INFO_CHUNKS] = c->n_chunks;
+  out[PV_INFO_LAUNCHES] = c->launches;
+  out[PV_INFO_RANK] = c->rank;
+  out[PV_INFO_WORLD] = c->world;
+  out[PV_INFO_DEVICE_BYTES] = (int64_t)c->device_bytes;
+  out[PV_INFO_NL_GLOBAL] = c->n_l_global;
+  API_END(c)
+}
+
+int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  std::vector<double> lm_local((size_t)c->n_ls * 4);
+  for (int j = 0; j < c->n_ls; ++j)
+    for (int q = 0; q < 4; ++q) lm_local[(size_t)j * 4 + q] = lms[c->lm_gid[j] * 4 + q];
+  double* dc = c->ctmp;  // n_p*12
+  CK(cudaMemcpyAsync(dc, cams, sizeof(double) * c->n_p * 12, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->tlm, lm_local.data(), sizeof(double) * lm_local.size(),
+                     cudaMemcpyHostToDevice, c->stream));
+  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
+  k_put_state<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, dc, c->tlm,
+                                                         c->crec, c->lrec);
+  c->launched();
+  c->check_launch();
+  c->sync();
+  c->lin_stage = 0;
+  c->vp_cached = false;
+  API_END(c)
+}
+
+static void get_state_impl(pv_ctx* c, const double* dcam, int cstride, const double* dlm,
+                           int lstride, double* cams, double* lms) {
+  double* tc = c->ctmp;
+  std::vector<double> lm_local((size_t)c->n_ls * 4);
+  double* tl = nullptr;
+  // gather into contiguous scratch (reuse cpart-sized buffers through a temp alloc)
+  tl = c->alloc<double>((size_t)c->n_ls * 4);
+  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
+  if (cstride == CREC) {
+    k_get_state<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, dcam, dlm, tc,
+                                                           tl);
+    c->launched();
+  } else {
+    CK(cudaMemcpyAsync(tc, dcam, sizeof(double) * c->n_p * 12, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(tl, dlm, sizeof(double) * c->n_ls * 4, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  }
+  (void)lstride;
+  CK(cudaMemcpyAsync(cams, tc, sizeof(double) * c->n_p * 12, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(lm_local.data(), tl, sizeof(double) * lm_local.size(),
+                     cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  // release the temporary
+  cudaFree(tl);
+  c->allocs.pop_back();
+  c->device_bytes -= std::max<size_t>((size_t)c->n_ls * 4, 1) * sizeof(double);
+  for (int j = 0; j < c->n_ls; ++j)
+    for (int q = 0; q < 4; ++q) lms[c->lm_gid[j] * 4 + q] = lm_local[(size_t)j * 4 + q];
+}
+
+int pv_get_state(pv_ctx* c, double* cams, double* lms) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  get_state_impl(c, c->crec, CREC, c->lrec, LREC, cams, lms);
+  API_END(c)
+}
+
+int pv_get_trial(pv_ctx* c, double* cams, double* lms) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  get_state_impl(c, c->tcam, 12, c->tlm, 4, cams, lms);
+  API_END(c)
+}
+
+int pv_cost(pv_ctx* c, int stage, int which, double* f) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (which != PV_CURRENT && which != PV_TRIAL) throw PvError(PV_EINVAL, "which");
+  STAGE_DISPATCH(stage, op_cost, c, which, f);
+  API_END(c)
+}
+
+int pv_linearize(pv_ctx* c, int stage) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  int rc = STAGE_DISPATCH(stage, op_linearize, c);
+  if (rc == PV_EDEGENERATE) c->err = "degenerate projection while linearizing stage 2";
+  return rc;
+  API_END(c)
+}
+
+int pv_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (!(lam >= 0.0)) throw PvError(PV_EINVAL, "damping must be non-negative");
+  if (c->lin_stage == 0) throw PvError(PV_EINVAL, "pv_damp before pv_linearize");
+  STAGE_DISPATCH(c->lin_stage, op_damp, c, lam, both, n_deg);
+  API_END(c)
+}
+
+int pv_power_solve(pv_ctx* c, int max_order, double thr, int* order, double* trunc) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (max_order < 0 || !(thr >= 0.0)) throw PvError(PV_EINVAL, "power series settings");
+  if (c->lin_stage == 0) throw PvError(PV_EINVAL, "pv_power_solve before pv_linearize");
+  int o = 0;
+  double t = 0.0;
+  STAGE_DISPATCH(c->lin_stage, op_power, c, max_order, thr, &o, &t);
+  if (order) *order = o;
+  if (trunc) *trunc = t;
+  API_END(c)
+}
+
+int pv_trial(pv_ctx* c, int stage, int* ok) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  int k = 0;
+  STAGE_DISPATCH(stage, op_trial, c, &k);
+  if (ok) *ok = k;
+  API_END(c)
+}
+
+int pv_accept(pv_ctx* c, int stage, int resolve, double* f_new, int64_t* n_rd) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (stage != 1 && stage != 2) throw PvError(PV_EINVAL, "stage");
+  if (resolve) {
+    if (stage != 1) throw PvError(PV_EINVAL, "landmark re-solve is a stage-1 operation");
+    op_resolve_trial(c, f_new, n_rd);
+  }
+  op_accept(c);
+  c->sync();
+  API_END(c)
+}
+
+int pv_resolve_current(pv_ctx* c, int64_t* n_rd) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
+  k_get_state<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, c->crec, c->lrec,
+                                                         c->tcam, c->tlm);
+  c->launched();
+  op_resolve_trial(c, nullptr, n_rd);
+  op_accept(c);
+  c->sync();
+  API_END(c)
+}
+
+int pv_get_step(pv_ctx* c, double* dx, double* dl) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (c->step_stage == 0) throw PvError(PV_EINVAL, "no step computed");
+  const int D = c->step_stage == 1 ? 12 : 11;
+  std::vector<double> x((size_t)c->n_p * 12), l((size_t)c->n_ls * 4);
+  CK(cudaMemcpyAsync(x.data(), c->cx, x.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(l.data(), c->ldl, l.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (dx)
+    for (int64_t i = 0; i < c->n_p; ++i)
+      for (int q = 0; q < D; ++q) dx[i * D + q] = x[i * 12 + q];
+  if (dl)
+    for (int j = 0; j < c->n_ls; ++j)
+      for (int q = 0; q < 3; ++q) dl[c->lm_gid[j] * 3 + q] = l[(size_t)j * 4 + q];
+  API_END(c)
+}
+
+}  // extern "C"
+
+template <int S>
+static void op_schur_apply(pv_ctx* c, const double* v, double* out) {
+  const int D = S == 1 ? 12 : 11;
+  std::vector<double> h((size_t)c->n_p * 12, 0.0);
+  for (int64_t i = 0; i < c->n_p; ++i)
+    for (int q = 0; q < D; ++q) h[i * 12 + q] = v[i * D + q];
+  CK(cudaMemcpyAsync(c->ctmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
+  k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->ctmp, c->ch, c->crec);
+  k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
+      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
+  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 0,
+                                                       c->coef);
+  c->launched(3);
+  launch_epilogue<S>(c, EPI_RAW, 0, 0.0);
+  c->check_launch();
+  CK(cudaMemcpyAsync(h.data(), c->cyr, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  for (int64_t i = 0; i < c->n_p; ++i)
+    for (int q = 0; q < D; ++q) out[i * D + q] = h[i * 12 + q];
+}
+
+extern "C" {
+
+int pv_schur_apply(pv_ctx* c, int stage, const double* v, double* out) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (c->lin_stage != stage) throw PvError(PV_EINVAL, "no linearization of that stage");
+  if (!c->vp_cached && c->lsys == nullptr) throw PvError(PV_EINVAL, "pv_damp first");
+  STAGE_DISPATCH(stage, op_schur_apply, c, v, out);
+  API_END(c)
+}
+
+}  // extern "C"
+
+template <int S>
+static void op_bench_terms(pv_ctx* c, int n, float* ms) {
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
+  float acc[4] = {0, 0, 0, 0};
+  for (int i = 1; i <= n; ++i) {
+    CK(cudaEventRecord(c->tev[0], c->stream));
+    k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
+        c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
+    CK(cudaEventRecord(c->tev[1], c->stream));
+    k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl,
+                                                         0, c->coef);
+    CK(cudaEventRecord(c->tev[2], c->stream));
+    c->launched(2);
+    launch_epilogue<S>(c, EPI_TERM, 1 << 20, -1.0);
+    CK(cudaEventRecord(c->tev[3], c->stream));
+    CK(cudaEventSynchronize(c->tev[3]));
+    float a, b, d;
+    CK(cudaEventElapsedTime(&a, c->tev[0], c->tev[1]));
+    CK(cudaEventElapsedTime(&b, c->tev[1], c->tev[2]));
+    CK(cudaEventElapsedTime(&d, c->tev[2], c->tev[3]));
+    acc[0] += a;
+    acc[1] += b;
+    acc[2] += d;
+    acc[3] += a + b + d;
+  }
+  for (int q = 0; q < 4; ++q) ms[q] = acc[q] / std::max(n, 1);
+}
+
+extern "C" {
+
+int pv_bench_terms(pv_ctx* c, int stage, int n, float* ms) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (c->lin_stage != stage) throw PvError(PV_EINVAL, "no linearization of that stage");
+  STAGE_DISPATCH(stage, op_bench_terms, c, n, ms);
+  API_END(c)
+}
+
+int pv_debug_get(pv_ctx* c, int which, double* out) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  auto down = [&](const double* src, size_t n) {
+    std::vector<double> h(n);
+    CK(cudaMemcpyAsync(h.data(), src, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return h;
+  };
+  const size_t np = c->n_p, nl = c->n_ls;
+  switch (which) {
+    case PV_DBG_U: {
+      auto h = down(c->cUd, np * 144);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_ULIN: {
+      auto h = down(c->cU, np * 144);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_UINV: {
+      auto h = down(c->cUi, np * 144);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_BP: {
+      auto h = down(c->cbp, np * 12);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_RHS: {
+      auto h = down(c->crhs, np * 12);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_X: {
+      auto h = down(c->cx, np * 12);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case PV_DBG_V: {
+      auto h = down(c->lvr, nl * 8);
+      for (size_t j = 0; j < nl; ++j)
+        for (int q = 0; q < 6; ++q) out[j * 6 + q] = h[j * 8 + q];
+      break;
+    }
+    case PV_DBG_VPINV:
+    case PV_DBG_DEGEN: {
+      auto h = down(c->lsys, nl * LSYS);
+      for (size_t j = 0; j < nl; ++j) {
+        if (which == PV_DBG_VPINV)
+          for (int q = 0; q < 6; ++q) out[j * 6 + q] = h[j * LSYS + q];
+        else
+          out[j] = h[j * LSYS + 6];
+      }
+      break;
+    }
+    case PV_DBG_BL:
+    case PV_DBG_DL: {
+      auto h = down(which == PV_DBG_BL ? c->lbl : c->ldl, nl * 4);
+      for (size_t j = 0; j < nl; ++j)
+        for (int q = 0; q < 3; ++q) out[j * 3 + q] = h[j * 4 + q];
+      break;
+    }
+    case PV_DBG_W: {
+      if (c->lin_stage == 0) throw PvError(PV_EINVAL, "no linearization");
+      double* w = c->alloc<double>((size_t)c->n_os * 36);
+      if (c->lin_stage == 1)
+        k_debug_w<1><<<blocks_for(nl, 128), 128, 0, c->stream>>>(c->g, c->crec, c->lrec, c->ch, w,
+                                                                  c->coef);
+      else
+        k_debug_w<2><<<blocks_for(nl, 128), 128, 0, c->stream>>>(c->g, c->crec, c->lrec, c->ch, w,
+                                                                  c->coef);
+      c->launched();
+      c->check_launch();
+      auto h = down(w, (size_t)c->n_os * 36);
+      std::copy(h.begin(), h.end(), out);
+      cudaFree(w);
+      c->allocs.pop_back();
+      c->device_bytes -= std::max<size_t>((size_t)c->n_os * 36, 1) * 8;
+      break;
+    }
+    default:
+      throw PvError(PV_EINVAL, "unknown debug buffer");
+  }
+  API_END(c)
+}
+
+}  // extern "C"

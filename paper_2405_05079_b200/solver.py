@@ -1,0 +1,354 @@
+"""Drop-in solver API of the PoVar hot path, running on the B200 through libpovar.so.
+
+Mirrors the reference entry points on this path (pkg/src/stratba):
+
+* ``lm_minimize``        -> solvers.py:318-393  (PoVar / PoBA stage 1, RiPoBA stage 2)
+* ``power_schur_solve``  -> solvers.py:126-150  (on a device ``SchurSystem``)
+* ``riemannian_step``    -> riemannian.py:125-138
+* ``assemble_system``    -> normal_eq.py:62-89 + riemannian.py:67-85 + normal_eq.py:156-198
+* ``total_cost``         -> objective.py:194-211
+* ``solve_landmarks``    -> objective.py:251-298
+* ``random_init``        -> bal_io.py:281-297
+
+The LM state machine (accept/reject, damping schedule, convergence test,
+trace records) stays in Python exactly as in the reference; every numeric
+step runs in hand-written sm_100a kernels.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .types import (BOTH, JOINT, POSE_ONLY, STAGE1, STAGE2, VARPRO, BaProblem,
+                    ConvergenceTrace, NumericFailureError, PoseConfig, ProjectiveState,
+                    SolverConfig, StepReport, TraceRecord, solver_label)
+
+
+class DeviceProblem:
+    """Device-resident observation graph + state of one landmark shard.
+
+    ``lm_range=(begin, end)`` restricts the context to landmarks
+    ``begin <= j < end`` (one rank of a sharded run); with ``world > 1`` every
+    method is collective over the NCCL world given by ``nccl_id``.
+    """
+
+    def __init__(self, problem: BaProblem, eta: float = 0.1, *, device: int | None = None,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 lm_range: tuple[int, int] | None = None):
+        lib = _lib.load()
+        PoseConfig(eta)  # validation (objective.py:45-47)
+        if device is None:
+            device = _default_device()
+        self.problem = problem
+        self.eta = float(eta)
+        self.device = int(device)
+        self.rank, self.world = int(rank), int(world)
+        b, e = lm_range if lm_range is not None else (0, problem.num_landmarks)
+        self.lm_range = (int(b), int(e))
+        ci = np.ascontiguousarray(problem.camera_indices, dtype=np.int64)
+        li = np.ascontiguousarray(problem.landmark_indices, dtype=np.int64)
+        m = np.ascontiguousarray(problem.measurements, dtype=np.float64)
+        ctx = ctypes.c_void_p()
+        rc = lib.pv_create(ctypes.byref(ctx), self.device, self.rank, self.world,
+                           nccl_id, problem.num_cameras, problem.num_landmarks,
+                           problem.num_observations, _lib.i64ptr(ci), _lib.i64ptr(li),
+                           _lib.dptr(m), self.lm_range[0], self.lm_range[1], self.eta)
+        _lib.check(rc, None)
+        self._ctx = ctx
+        self._lib = lib
+        self._finalizer = weakref.finalize(self, lib.pv_destroy, ctx)
+        info = self.info()
+        self.n_p = int(info["n_p"])
+        self.n_l_local = int(info["n_l_local"])
+        self.n_o_local = int(info["n_o_local"])
+        self._state_template = None
+
+    # -- plumbing -----------------------------------------------------------
+    def _call(self, name, *args):
+        _lib.check(getattr(self._lib, name)(self._ctx, *args), self._ctx)
+
+    def close(self):
+        self._finalizer()
+
+    def info(self) -> dict:
+        out = np.zeros(_lib.PV_INFO_COUNT, dtype=np.int64)
+        self._call("pv_info", _lib.i64ptr(out))
+        return {k: int(out[i]) for i, k in enumerate(_lib.INFO_FIELDS)}
+
+    @property
+    def stream_handle(self) -> int:
+        return int(self._lib.pv_stream(self._ctx) or 0)
+
+    # -- state ----------------------------------------------------------------
+    def set_state(self, state: ProjectiveState) -> None:
+        cams = np.ascontiguousarray(state.cameras, dtype=np.float64)
+        lms = np.ascontiguousarray(state.landmarks, dtype=np.float64)
+        if cams.shape != (self.n_p, 3, 4) or lms.shape != (self.problem.num_landmarks, 4):
+            raise ValueError("state does not match the problem")
+        self._call("pv_set_state", _lib.dptr(cams), _lib.dptr(lms))
+        self._state_template = lms
+
+    def get_state(self, trial: bool = False) -> ProjectiveState:
+        cams = np.empty((self.n_p, 3, 4))
+        lms = np.array(self._state_template, copy=True)
+        self._call("pv_get_trial" if trial else "pv_get_state", _lib.dptr(cams), _lib.dptr(lms))
+        return ProjectiveState(cams, lms)
+
+    # -- numeric steps ----------------------------------------------------------
+    def cost(self, stage: int, trial: bool = False) -> float:
+        f = ctypes.c_double()
+        self._call("pv_cost", int(stage), _lib.PV_TRIAL if trial else _lib.PV_CURRENT,
+                   ctypes.byref(f))
+        return f.value
+
+    def linearize(self, stage: int) -> None:
+        self._call("pv_linearize", int(stage))
+
+    def damp(self, lam: float, both: bool) -> int:
+        n = ctypes.c_int64()
+        self._call("pv_damp", float(lam), int(bool(both)), ctypes.byref(n))
+        return n.value
+
+    def power_solve(self, max_order: int, threshold: float) -> tuple[int, float]:
+        order, trunc = ctypes.c_int(), ctypes.c_double()
+        self._call("pv_power_solve", int(max_order), float(threshold), ctypes.byref(order),
+                   ctypes.byref(trunc))
+        return order.value, trunc.value
+
+    def trial(self, stage: int) -> bool:
+        ok = ctypes.c_int()
+        self._call("pv_trial", int(stage), ctypes.byref(ok))
+        return bool(ok.value)
+
+    def accept(self, stage: int, resolve: bool) -> tuple[float, int]:
+        f, n = ctypes.c_double(math.nan), ctypes.c_int64()
+        self._call("pv_accept", int(stage), int(bool(resolve)), ctypes.byref(f), ctypes.byref(n))
+        return f.value, n.value
+
+    def resolve_current(self) -> int:
+        n = ctypes.c_int64()
+        self._call("pv_resolve_current", ctypes.byref(n))
+        return n.value
+
+    def step(self, stage: int) -> tuple[np.ndarray, np.ndarray]:
+        d = 12 if stage == STAGE1 else 11
+        dx = np.zeros(self.n_p * d)
+        dl = np.zeros(self.problem.num_landmarks * 3)
+        self._call("pv_get_step", _lib.dptr(dx), _lib.dptr(dl))
+        return dx, dl
+
+    def schur_apply(self, stage: int, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(v)
+        self._call("pv_schur_apply", int(stage), _lib.dptr(v), _lib.dptr(out))
+        return out
+
+    def bench_terms(self, stage: int, n_terms: int) -> dict:
+        ms = (ctypes.c_float * 4)()
+        self._call("pv_bench_terms", int(stage), int(n_terms), ms)
+        return {"phase1_ms": ms[0], "phase2_ms": ms[1], "epilogue_ms": ms[2], "term_ms": ms[3]}
+
+    def debug(self, which: int) -> np.ndarray:
+        sizes = {_lib.PV_DBG_U: (self.n_p, 144), _lib.PV_DBG_ULIN: (self.n_p, 144),
+                 _lib.PV_DBG_UINV: (self.n_p, 144), _lib.PV_DBG_BP: (self.n_p, 12),
+                 _lib.PV_DBG_RHS: (self.n_p, 12), _lib.PV_DBG_X: (self.n_p, 12),
+                 _lib.PV_DBG_V: (self.n_l_local, 6), _lib.PV_DBG_VPINV: (self.n_l_local, 6),
+                 _lib.PV_DBG_BL: (self.n_l_local, 3), _lib.PV_DBG_DL: (self.n_l_local, 3),
+                 _lib.PV_DBG_DEGEN: (self.n_l_local,), _lib.PV_DBG_W: (self.n_o_local, 36)}
+        out = np.zeros(sizes[which])
+        self._call("pv_debug_get", int(which), _lib.dptr(out))
+        return out
+
+
+def _default_device() -> int:
+    import os
+    return int(os.environ.get("LOCAL_RANK", "0")) if "LOCAL_RANK" in os.environ else 0
+
+
+# one cached context per live problem object (BaProblem is immutable)
+_CONTEXTS: dict = {}
+
+
+def device_problem(problem: BaProblem, eta: float = 0.1) -> DeviceProblem:
+    key = (id(problem), float(eta))
+    hit = _CONTEXTS.get(key)
+    if hit is not None and hit[0]() is problem:
+        return hit[1]
+    dp = DeviceProblem(problem, eta)
+    _CONTEXTS[key] = (weakref.ref(problem, lambda _r, k=key: _CONTEXTS.pop(k, None)), dp)
+    return dp
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped API
+
+
+def total_cost(state: ProjectiveState, problem: BaProblem, stage: int,
+               config: PoseConfig | None = None, *, dp: DeviceProblem | None = None) -> float:
+    """objective.py:194-211 on the device (+inf for a degenerate stage-2 state)."""
+    if stage not in (STAGE1, STAGE2):
+        raise ValueError(f"unknown stage {stage!r}")
+    dp = dp or device_problem(problem, (config or PoseConfig()).eta)
+    dp.set_state(state)
+    return dp.cost(stage)
+
+
+def solve_landmarks(state: ProjectiveState, problem: BaProblem,
+                    config: PoseConfig | None = None, *, dp: DeviceProblem | None = None
+                    ) -> np.ndarray:
+    """Closed-form stage-1 landmarks (objective.py:251-298) on the device."""
+    if problem.num_observations == 0:
+        return np.array(state.landmarks, copy=True)
+    dp = dp or device_problem(problem, (config or PoseConfig()).eta)
+    dp.set_state(state)
+    n_bad = dp.resolve_current()
+    if n_bad:
+        import logging
+        logging.getLogger(__name__).warning(
+            "left %d landmarks unchanged: rank-deficient closed-form systems", n_bad)
+    return np.array(dp.get_state().landmarks)
+
+
+def random_init(problem: BaProblem, seed: int, config: PoseConfig | None = None
+                ) -> ProjectiveState:
+    """Philox N(0,1) cameras + closed-form landmarks (bal_io.py:281-297)."""
+    rng = np.random.Generator(np.random.Philox(int(seed) & 0xFFFFFFFFFFFFFFFF))
+    cams = rng.standard_normal((problem.num_cameras, 3, 4))
+    zero = np.zeros((problem.num_landmarks, 4))
+    zero[:, 3] = 1.0
+    lms = solve_landmarks(ProjectiveState(cams, zero), problem, config)
+    return ProjectiveState(cams, lms)
+
+
+class SchurSystem:
+    """Handle on a damped block system living on the device (normal_eq.py:109-142)."""
+
+    def __init__(self, dp: DeviceProblem, stage: int, lam: float, damping_mode: str):
+        self.dp, self.stage, self.lam, self.damping_mode = dp, stage, lam, damping_mode
+        self.n_degenerate = 0
+
+    @property
+    def n_cameras(self) -> int:
+        return self.dp.n_p
+
+    @property
+    def pose_width(self) -> int:
+        return 12 if self.stage == STAGE1 else 11
+
+    @property
+    def pose_dim(self) -> int:
+        return self.n_cameras * self.pose_width
+
+
+def assemble_system(problem: BaProblem, state: ProjectiveState, stage: int, lam: float,
+                    damping_mode: str = POSE_ONLY, config: PoseConfig | None = None, *,
+                    dp: DeviceProblem | None = None) -> SchurSystem:
+    """Linearize + assemble on the device (normal_eq.py:62-89,156-198; riemannian.py:67-85)."""
+    if lam < 0:
+        raise ValueError("damping must be non-negative")
+    if damping_mode not in (POSE_ONLY, BOTH):
+        raise ValueError(f"unknown damping mode {damping_mode!r}")
+    dp = dp or device_problem(problem, (config or PoseConfig()).eta)
+    dp.set_state(state)
+    dp.linearize(stage)
+    sysm = SchurSystem(dp, stage, lam, damping_mode)
+    sysm.n_degenerate = dp.damp(lam, damping_mode == BOTH)
+    return sysm
+
+
+def power_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
+    """solvers.py:126-150 on a device system; returns host update vectors."""
+    order, trunc = system.dp.power_solve(config.max_power_order, config.power_threshold)
+    dx, dl = system.dp.step(system.stage)
+    return StepReport(dx, dl, order, order, trunc)
+
+
+def riemannian_step(problem: BaProblem, state: ProjectiveState, config: SolverConfig,
+                    lam: float | None = None, bases=None, *, dp: DeviceProblem | None = None
+                    ) -> StepReport:
+    """riemannian.py:125-138: tangent-space reduced solve (11 per camera, 3 per landmark).
+
+    ``bases`` is accepted for signature compatibility; the device derives the
+    same Householder bases (riemannian.py:37-56) from ``state``.
+    """
+    if config.inner_solver != "power":
+        raise NotImplementedError("only the power-series inner solver runs on the GPU path")
+    if lam is None:
+        lam = config.initial_lambda
+    system = assemble_system(problem, state, STAGE2, lam, BOTH, config.pose, dp=dp)
+    return power_schur_solve(system, config)
+
+
+def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: SolverConfig,
+                trace_sink=None, *, solver_id: str | None = None, problem_id: str = "",
+                dp: DeviceProblem | None = None, decisions: list | None = None
+                ) -> tuple[ProjectiveState, ConvergenceTrace]:
+    """Levenberg-Marquardt outer loop (solvers.py:318-393) over device steps.
+
+    Same accept rule (strict decrease), damping schedule, convergence test and
+    trace records as the reference.  A rejected step leaves the state
+    unchanged, so the linearization is reused (results-identical, SURVEY
+    App. A.6).  ``decisions`` (optional list) receives one dict per iteration
+    (lam, f_trial, accepted, power order) for parity checks.
+    """
+    if stage not in (STAGE1, STAGE2):
+        raise ValueError(f"unknown stage {stage!r}")
+    if config.inner_solver != "power":
+        raise NotImplementedError(
+            f"inner_solver={config.inner_solver!r}: only the power series runs on the GPU path")
+    pose = config.pose
+    dp = dp or device_problem(problem, pose.eta)
+    dp.set_state(state)
+    f = dp.cost(stage)
+    if not math.isfinite(f):
+        raise NumericFailureError(f"stage {stage} starting cost is not finite")
+    label = solver_id if solver_id is not None else solver_label(stage, config)
+    stage_name = "stage1" if stage == STAGE1 else "stage2"
+    varpro = config.mode == VARPRO
+    both = stage == STAGE2 or not varpro
+    t0 = time.perf_counter()
+    records = [TraceRecord(0, f, 0.0)]
+    if trace_sink is not None:
+        trace_sink(records[0])
+    lam = config.initial_lambda
+    linearized = False
+    for it in range(1, config.max_outer_iterations + 1):
+        if not linearized:
+            dp.linearize(stage)  # FloatingPointError on a degenerate stage-2 point
+            linearized = True
+        dp.damp(lam, both)
+        order, _trunc = dp.power_solve(config.max_power_order, config.power_threshold)
+        ok = dp.trial(stage)
+        f_trial = dp.cost(stage, trial=True) if ok else math.inf
+        converged = False
+        accepted = f_trial < f
+        if accepted:
+            if stage == STAGE1 and varpro:
+                f_trial, _ = dp.accept(stage, resolve=True)
+            else:
+                dp.accept(stage, resolve=False)
+            linearized = False
+            converged = abs(f - f_trial) / (f if f > 0 else 1.0) <= config.function_tolerance
+            f = f_trial
+            lam = max(config.lambda_min, lam * config.lambda_decrease)
+        else:
+            if math.isfinite(f_trial):
+                converged = abs(f - f_trial) / (f if f > 0 else 1.0) <= config.function_tolerance
+            lam = min(config.lambda_max, lam * config.lambda_increase)
+        if decisions is not None:
+            decisions.append(dict(iteration=it, f_trial=f_trial, accepted=accepted, order=order,
+                                  lam_next=lam))
+        rec = TraceRecord(it, f, time.perf_counter() - t0)
+        records.append(rec)
+        if trace_sink is not None:
+            trace_sink(rec)
+        if converged:
+            break
+    final = dp.get_state()
+    return final, ConvergenceTrace(label, problem_id, stage_name, records, records[0].cost)
