@@ -1,0 +1,382 @@
+"""PoVar hot-path benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[4], the config the metric's target is quoted
+on; it fits one B200): the seeded 13,682-camera / 4,456,117-landmark /
+~29.0M-observation synthetic problem, fp64, stage-1 PoVar (varpro + power
+series, <= 30 terms, threshold 0.01), random N(0,1) start.
+
+* a "step" = one full stage-1 LM iteration (linearize, damp, power series,
+  back-substitution, trial, cost, accept + closed-form landmark re-solve)
+  continuing an LM run; ``value`` = n_obs x iterations/s (obs/s), inputs
+  resident in HBM.
+* ``spmv`` = the S'.v term alone (the power-series unit of work).
+* ``roofline`` = the dominant term kernel, algorithmic bytes / mean launch
+  time from CUDA events inside this run.
+* ``e2e`` = the public ``lm_minimize`` call with host state in / out
+  (one iteration per call), i.e. host<->device copies inside the timing.
+* ``--impl reference`` times the CPU oracle port (oracle/povar_oracle.py, the
+  NumPy restatement of the reference) on a landmark-subsampled slice.
+
+Multi-GPU: ``torchrun --nproc-per-node N bench.py --gpus N``: landmarks are
+sharded across ranks (equal observation counts), cameras replicated, one NCCL
+allreduce of the camera vector per term; timings are max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "power-series S'x mat-vecs/s and LM iters/s (obs/s); % of HBM roofline"
+CONFIG = "vlarge"
+CPU_SAMPLE_FRACTION = 0.01  # landmark fraction of vlarge timed on the CPU (~290k obs)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def term_bytes(n_p, n_l, n_o, stage=1):
+    """Algorithmic (compulsory) DRAM bytes of one term per kernel, DESIGN.md section 5."""
+    n_chunks = n_o / 256.0 + n_p
+    p1 = 20 * n_o + (32 + 48 + 32 + 4 + 4) * n_l + 192 * n_p
+    p2 = 20 * n_o + 64 * n_l + 96 * n_p + (96 + 12) * n_chunks
+    ep = (1152 + 96 + 96 + 96 + 16) * n_p + 96 * n_chunks
+    r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
+    return {"phase1": p1, "phase2": p2, "epilogue": ep, "r1_term": r1}
+
+
+def cpu_port_lm(fraction, iters=2, seed=0):
+    """Time the oracle port (NumPy restatement of the reference) on a slice."""
+    from oracle import povar_oracle as O
+    from paper_2405_05079_b200 import synth
+    problem, _ = synth.make_problem(CONFIG, seed, landmark_fraction=fraction)
+    state = synth.random_state(problem, 1)
+    g = O.graph_of(problem)
+    cams, lms = np.array(state.cameras), np.array(state.landmarks)
+    O.lm_minimize(g, cams, lms, 1, max_iterations=1, max_order=30, ftol=1e-300)  # warm
+    t = time.perf_counter()
+    log = O.lm_minimize(g, cams, lms, 1, max_iterations=iters, max_order=30, ftol=1e-300)
+    dt = (time.perf_counter() - t) / max(1, len(log.decisions))
+    return problem.num_observations / dt, dt, problem
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    fr = CPU_SAMPLE_FRACTION
+    from oracle import povar_oracle as O
+    from paper_2405_05079_b200 import synth
+    problem, _ = synth.make_problem(CONFIG, 0, landmark_fraction=fr)
+    state = synth.random_state(problem, 1)
+    g = O.graph_of(problem)
+    cams, lms = np.array(state.cameras), np.array(state.landmarks)
+    # warmup + timed LM iterations of the NumPy port, continuing one LM run
+    log = O.lm_minimize(g, cams, lms, 1, max_iterations=max(1, args.warmup), max_order=30,
+                        ftol=1e-300)
+    cams, lms = log.cams, log.lms
+    t = time.perf_counter()
+    log = O.lm_minimize(g, cams, lms, 1, max_iterations=args.steps, max_order=30, ftol=1e-300)
+    dt = time.perf_counter() - t
+    n_it = len(log.decisions)
+    value = problem.num_observations * n_it / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "obs/s",
+            "n_gpus": world, "steps": n_it, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / n_it, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE vlarge generator, landmark-subsampled)",
+            "config": {"workload": "vlarge stage-1 PoVar LM iteration (CPU oracle port)",
+                       "landmark_fraction": fr, "n_cameras": problem.num_cameras,
+                       "n_landmarks": problem.num_landmarks,
+                       "n_obs": problem.num_observations, "max_power_order": 30},
+            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": 1, "kind": "port",
+                             "sample": f"{fr:.0%} of vlarge landmarks "
+                                       f"({problem.num_observations} obs), {n_it} LM iterations"},
+            "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stage2", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_05079_b200 as pv
+    from paper_2405_05079_b200 import shard, synth
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = synth.CONFIGS[args.config]
+    problem, _ = synth.make_problem(args.config, 0)
+    state0 = synth.random_state(problem, 1)
+    n_p, n_l, n_o = problem.num_cameras, problem.num_landmarks, problem.num_observations
+    plan = shard.plan_shards(problem, world)
+    nccl_id = shard.broadcast_nccl_id(rank, world) if world > 1 else None
+    dp = pv.DeviceProblem(problem, 0.1, device=local, rank=rank, world=world, nccl_id=nccl_id,
+                          lm_range=plan[rank])
+    stream = torch.cuda.ExternalStream(dp.stream_handle, device=local)
+    scfg = pv.SolverConfig(max_outer_iterations=1, max_power_order=cfg.max_power_order,
+                           function_tolerance=1e-300)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- LM iterations (value) -------------------------------------------------
+    dp.set_state(state0)
+    f = dp.cost(1)
+    lam = scfg.initial_lambda
+    orders = []
+
+    def lm_iteration():
+        nonlocal f, lam
+        dp.linearize(1)
+        dp.damp(lam, False)
+        order, _ = dp.power_solve(scfg.max_power_order, scfg.power_threshold)
+        orders.append(order)
+        ok = dp.trial(1)
+        ft = dp.cost(1, trial=True) if ok else math.inf
+        if ft < f:
+            f, _ = dp.accept(1, resolve=True)
+            lam = max(scfg.lambda_min, lam * scfg.lambda_decrease)
+        else:
+            lam = min(scfg.lambda_max, lam * scfg.lambda_increase)
+
+    for _ in range(args.warmup):
+        lm_iteration()
+    orders.clear()
+    launches0 = dp.info()["launches"]
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            lm_iteration()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    launches = dp.info()["launches"] - launches0
+    ms_step = ms_total / args.steps
+    value = n_o * args.steps / (ms_total * 1e-3)
+
+    # ---- S'.v terms and per-kernel roofline ------------------------------------
+    dp.linearize(1)
+    dp.damp(lam, False)
+    dp.power_solve(1, 0.0)
+    dp.bench_terms(1, 3)
+    barrier()
+    kt = dp.bench_terms(1, 20)
+    kt = {k: max_over_ranks(v) for k, v in kt.items()}
+    peak, peak_src = _peaks()
+    loc = dp.info()
+    tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], 1)
+    kern = {}
+    for name, key in (("k_phase1", "phase1"), ("k_phase2", "phase2"), ("k_epilogue", "epilogue")):
+        ms = kt[f"{key}_ms"]
+        gbs = tb[key] / (ms * 1e-3) / 1e9
+        kern[name] = {"ms": ms, "algorithmic_bytes": tb[key], "achieved_gbs": gbs,
+                      "frac": gbs / peak}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    term_ms = kt["term_ms"]
+    spmv = {"ms_per_term": term_ms, "terms_per_s": 1e3 / term_ms,
+            "obs_per_s": n_o / (term_ms * 1e-3),
+            "r1_equivalent_gbs": tb["r1_term"] * world / (term_ms * 1e-3) / 1e9,
+            "r1_equivalent_frac": tb["r1_term"] * world / (term_ms * 1e-3) / 1e9 / peak,
+            "r1_equivalent_frac_of_8tbs": tb["r1_term"] * world / (term_ms * 1e-3) / 8e12,
+            "kernels": kern}
+    roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": None, "kernel": dom,
+                "peak_source": peak_src}
+
+    # ---- stage 2 (RiPoBA) iteration throughput from the lifted state ------------
+    stage2 = None
+    if not args.no_stage2:
+        try:
+            s1 = dp.get_state()
+            lifted = pv.lift_stage1_to_stage2(s1)
+            dp.set_state(lifted)
+            f2 = dp.cost(2)
+            if math.isfinite(f2):
+                lam2 = scfg.initial_lambda
+
+                def it2():
+                    nonlocal f2, lam2
+                    dp.linearize(2)
+                    dp.damp(lam2, True)
+                    dp.power_solve(scfg.max_power_order, scfg.power_threshold)
+                    ok = dp.trial(2)
+                    ft = dp.cost(2, trial=True) if ok else math.inf
+                    if ft < f2:
+                        dp.accept(2, resolve=False)
+                        f2 = ft
+                        lam2 = max(scfg.lambda_min, lam2 * scfg.lambda_decrease)
+                    else:
+                        lam2 = min(scfg.lambda_max, lam2 * scfg.lambda_increase)
+                it2()
+                barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                n2 = max(3, args.steps // 2)
+                a.record(stream)
+                for _ in range(n2):
+                    it2()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms2 = max_over_ranks(a.elapsed_time(b)) / n2
+                dp.linearize(2)
+                dp.damp(lam2, True)
+                kt2 = dp.bench_terms(2, 10)
+                stage2 = {"ms_per_iter": ms2, "obs_per_s": n_o / (ms2 * 1e-3),
+                          "ms_per_term": max_over_ranks(kt2["term_ms"])}
+        except Exception as e:  # report, do not fail the stage-1 line
+            stage2 = {"error": f"{type(e).__name__}: {e}"}
+
+    # ---- e2e through the public API (host state in/out, one iteration per call) --
+    e2e = None
+    if not args.no_e2e:
+        st = dp.get_state() if stage2 is None else None
+        st = st or state0
+        cfg1 = pv.SolverConfig(max_outer_iterations=1, max_power_order=cfg.max_power_order,
+                               function_tolerance=1e-300)
+        st, _ = pv.lm_minimize(problem, st, 1, cfg1, dp=dp)  # warm
+        barrier()
+        t = time.perf_counter()
+        n_e = max(3, args.steps // 2)
+        for _ in range(n_e):
+            st, _tr = pv.lm_minimize(problem, st, 1, cfg1, dp=dp)
+        dt = max_over_ranks(time.perf_counter() - t)
+        bytes_state = st.cameras.nbytes + st.landmarks.nbytes
+        e2e = {"value": n_o * n_e / dt, "unit": "obs/s", "h2d_bytes_per_step": bytes_state,
+               "d2h_bytes_per_step": bytes_state + 8, "ms_per_step": 1e3 * dt / n_e,
+               "api": "paper_2405_05079_b200.lm_minimize(max_outer_iterations=1)"}
+
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, sp = cpu_port_lm(CPU_SAMPLE_FRACTION, iters=2)
+        cpu = {"value": v, "unit": "obs/s", "cores": 1, "kind": "port",
+               "sample": f"{CPU_SAMPLE_FRACTION:.0%} of vlarge landmarks "
+                         f"({sp.num_observations} obs), 2 stage-1 LM iterations, "
+                         f"{dt:.2f} s/iter, NumPy oracle port single-threaded"}
+
+    if rank == 0:
+        ws = (dp.info()["device_bytes"]) / 1e9
+        line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64",
+                "data": "synthetic (seeded BASELINE vlarge generator, SURVEY App. C)",
+                "config": {"workload": f"{args.config} stage-1 PoVar LM iteration",
+                           "n_cameras": n_p, "n_landmarks": n_l, "n_obs": n_o,
+                           "max_power_order": cfg.max_power_order, "power_threshold": 0.01,
+                           "mean_power_order": float(np.mean(orders)) if orders else None,
+                           "l2": f"inputs larger than L2 (device working set {ws:.1f} GB)",
+                           "parallelism": f"landmark-sharded dp{world}"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary(), "spmv": spmv,
+                "stage2": stage2}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
