@@ -107,13 +107,20 @@ class ClockSampler:
 
 
 def term_bytes(n_p, n_l, n_o, stage=1):
-    """Algorithmic (compulsory) DRAM bytes of one term per kernel, DESIGN.md section 5."""
-    n_chunks = n_o / 256.0 + n_p
-    p1 = 20 * n_o + (32 + 48 + 32 + 4 + 4) * n_l + 192 * n_p
-    p2 = 20 * n_o + 64 * n_l + 96 * n_p + (96 + 12) * n_chunks
-    ep = (1152 + 96 + 96 + 96 + 16) * n_p + 96 * n_chunks
+    """Algorithmic (compulsory) DRAM bytes of one power-series term per kernel.
+
+    DESIGN.md section 5: every array element a kernel must touch, counted once.
+    k_lm_reduce streams s (32 B/obs) and the landmark->camera-order map (4 B/obs),
+    scatters t into the camera-sorted slot of every observation (32 B/obs), and
+    per landmark reads the task descriptor, V+ (2 x 32 B sectors), b/x.  k_cam
+    streams the camera-sorted t (32), x (32), m (16), landmark-sorted position
+    (4) and scatters s (32) per observation, plus per camera P, U^-1 and the
+    small vectors (~1.6 KB).
+    """
+    lmr = 36 * n_o + 32 * n_o + (104 if stage == 1 else 136) * n_l
+    cam = 116 * n_o + 1600 * n_p
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
-    return {"phase1": p1, "phase2": p2, "epilogue": ep, "r1_term": r1}
+    return {"lm_reduce": lmr, "cam": cam, "r1_term": r1}
 
 
 def cpu_port_lm(fraction, iters=2, seed=0):
@@ -269,8 +276,9 @@ def main():
     loc = dp.info()
     tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], 1)
     kern = {}
-    for name, key in (("k_phase1", "phase1"), ("k_phase2", "phase2"), ("k_epilogue", "epilogue")):
-        ms = kt[f"{key}_ms"]
+    for name, key, tkey in (("k_lm_reduce", "lm_reduce", "phase1_ms"),
+                            ("k_cam", "cam", "phase2_ms")):
+        ms = kt[tkey]
         gbs = tb[key] / (ms * 1e-3) / 1e9
         kern[name] = {"ms": ms, "algorithmic_bytes": tb[key], "achieved_gbs": gbs,
                       "frac": gbs / peak}

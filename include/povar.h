@@ -65,6 +65,14 @@ enum {
   PV_INFO_DEVICE_BYTES = 8, PV_INFO_NL_GLOBAL = 9, PV_INFO_COUNT = 16
 };
 
+/* tuning knobs of the term kernels (pv_set_option); results do not depend on them */
+enum {
+  PV_OPT_STAGE_CAP = 0,   /* observations per camera staged in shared memory (0..2048)     */
+  PV_OPT_POL_STREAM = 1,  /* L2 priority of camera-sorted streams: 0 normal 1 first 2 last */
+  PV_OPT_POL_T = 2,       /* L2 priority of the gathered landmark vectors t              */
+  PV_OPT_POL_S = 3        /* L2 priority of the per-observation partials s               */
+};
+
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the
  * host broadcasts it (torch.distributed store) before pv_create. */
 int pv_nccl_unique_id(unsigned char out[128]);
@@ -82,6 +90,7 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
 void pv_destroy(pv_ctx* ctx);
 const char* pv_last_error(pv_ctx* ctx); /* ctx may be NULL (thread-local create error) */
 int pv_info(pv_ctx* ctx, int64_t* out /* PV_INFO_COUNT */);
+int pv_set_option(pv_ctx* ctx, int key, int64_t value);
 /* cudaStream_t of the context, for event timing by the caller */
 void* pv_stream(pv_ctx* ctx);
 

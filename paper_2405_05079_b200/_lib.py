@@ -21,6 +21,7 @@ PV_CURRENT, PV_TRIAL = 0, 1
 INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
                "device_bytes", "n_l_global")
 PV_INFO_COUNT = 16
+PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S = range(4)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
 _P = ctypes.c_void_p
@@ -36,6 +37,7 @@ SIGNATURES = [
     ("pv_last_error", ctypes.c_char_p, [_P]),
     ("pv_info", ctypes.c_int, [_P, _I64]),
     ("pv_stream", _P, [_P]),
+    ("pv_set_option", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64]),
     ("pv_set_state", ctypes.c_int, [_P, _D, _D]),
     ("pv_get_state", ctypes.c_int, [_P, _D, _D]),
     ("pv_get_trial", ctypes.c_int, [_P, _D, _D]),

@@ -60,26 +60,26 @@ struct pv_ctx {
   std::vector<void*> allocs;
 
   int64_t n_p = 0, n_l_global = 0, n_o_global = 0;
-  int n_ls = 0, n_os = 0, n_tasks = 0, n_chunks = 0;
+  int n_ls = 0, n_os = 0, n_tasks = 0;
   std::vector<int64_t> lm_gid;  // local -> global landmark id
   Coef coef{};
 
   // graph (device)
   Graph g{};
   int *d_ls_cam = nullptr, *d_lm_off = nullptr, *d_task_lm = nullptr, *d_cs_lm = nullptr,
-      *d_chunk_off = nullptr, *d_chunk_cam = nullptr, *d_cam_chunk = nullptr;
+      *d_cs_pos = nullptr, *d_cam_off = nullptr, *d_ls2cs = nullptr;
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
-  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam;
-  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cyc, *cyr, *lin_part, *cUraw, *nrm, *cpart,
-      *ctmp, *scal;
+  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam, *tarr, *cs_x, *sbuf;
+  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
   int* flags;
   unsigned* ticket;
   PowerCtl* ctl;
   PowerCtl* host_ctl = nullptr;  // mapped pinned mirror
   PowerCtl* host_ctl_dev = nullptr;
 
+  Tune tune{1792, 0, 0, 0};
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
   int step_stage = 0;
@@ -107,8 +107,6 @@ struct pv_ctx {
   void sync() { CK(cudaStreamSynchronize(stream)); }
 
   int nblk_tasks() const { return blocks_for((long long)n_tasks * 32, 256); }
-  int nblk_chunks() const { return blocks_for((long long)n_chunks * 32, 256); }
-  int nblk_epi() const { return blocks_for(n_p * 16, 256); }
 };
 
 // ---------------------------------------------------------------------------
@@ -172,53 +170,51 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   std::vector<int> cam_off(n_p + 1, 0);
   for (int64_t k = 0; k < n_os; ++k) cam_off[ls_cam[k] + 1]++;
   for (int64_t i = 0; i < n_p; ++i) cam_off[i + 1] += cam_off[i];
-  std::vector<int> cs_lm(n_os);
+  std::vector<int> cs_lm(n_os), cs_pos(n_os), ls2cs(n_os);
   std::vector<double> cs_m(2 * n_os);
   {
     std::vector<int> pos(cam_off.begin(), cam_off.end() - 1);
     for (int64_t k = 0; k < n_os; ++k) {
       int p = pos[ls_cam[k]]++;
       cs_lm[p] = ls_lid[k];
+      cs_pos[p] = (int)k;
+      ls2cs[k] = p;
       cs_m[2 * p] = ls_m[2 * k];
       cs_m[2 * p + 1] = ls_m[2 * k + 1];
     }
   }
-  // camera chunks
-  std::vector<int> chunk_off, chunk_cam, cam_chunk(n_p + 1, 0);
-  for (int64_t i = 0; i < n_p; ++i) {
-    cam_chunk[i] = (int)chunk_cam.size();
-    for (int s = cam_off[i]; s < cam_off[i + 1]; s += PV_CHUNK) {
-      chunk_off.push_back(s);
-      chunk_cam.push_back((int)i);
-    }
-  }
-  cam_chunk[n_p] = (int)chunk_cam.size();
-  chunk_off.push_back((int)n_os);
-  // landmark tasks: whole landmarks packed into <= 32 lanes, or one long landmark
-  std::vector<int> task_lm;
+  // landmark tasks: whole landmarks packed into <= 32 lanes, or one long landmark;
+  // descriptor {first obs, obs count, first landmark, segment-head lane mask}
+  std::vector<int> task_desc;
   {
     int j = 0;
     while (j < n_ls) {
-      task_lm.push_back(j);
+      const int l0 = j;
+      const int o0 = lm_off[j];
       int k = lm_off[j + 1] - lm_off[j];
+      unsigned heads = 1u;
       if (k > 32) {
         ++j;
-        continue;
-      }
-      int total = k, nl = 1;
-      ++j;
-      while (j < n_ls && nl < 32) {
-        int kk = lm_off[j + 1] - lm_off[j];
-        if (kk > 32 || total + kk > 32) break;
-        total += kk;
-        ++nl;
+      } else {
+        int total = k, nl = 1;
         ++j;
+        while (j < n_ls && nl < 32) {
+          int kk = lm_off[j + 1] - lm_off[j];
+          if (kk > 32 || total + kk > 32) break;
+          heads |= 1u << total;
+          total += kk;
+          ++nl;
+          ++j;
+        }
+        k = total;
       }
+      task_desc.push_back(o0);
+      task_desc.push_back(k);
+      task_desc.push_back(l0);
+      task_desc.push_back((int)heads);
     }
-    task_lm.push_back(n_ls);
   }
-  c->n_tasks = (int)task_lm.size() - 1;
-  c->n_chunks = (int)chunk_cam.size();
+  c->n_tasks = (int)task_desc.size() / 4;
 
   auto up_i = [&](const std::vector<int>& v) {
     int* d = c->alloc<int>(v.size());
@@ -234,12 +230,14 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->d_ls_cam = up_i(ls_cam);
   c->d_ls_m = up_d(ls_m);
   c->d_lm_off = up_i(lm_off);
-  c->d_task_lm = up_i(task_lm);
+  c->d_task_lm = up_i(task_desc);
+  cs_lm.resize(cs_lm.size() + 8, 0);
+  cs_pos.resize(cs_pos.size() + 8, 0);
   c->d_cs_lm = up_i(cs_lm);
   c->d_cs_m = up_d(cs_m);
-  c->d_chunk_off = up_i(chunk_off);
-  c->d_chunk_cam = up_i(chunk_cam);
-  c->d_cam_chunk = up_i(cam_chunk);
+  c->d_cs_pos = up_i(cs_pos);
+  c->d_cam_off = up_i(cam_off);
+  c->d_ls2cs = up_i(ls2cs);
   c->sync();  // host vectors go out of scope
 
   Graph& g = c->g;
@@ -247,16 +245,15 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   g.n_l = n_ls;
   g.n_o = (int)n_os;
   g.n_tasks = c->n_tasks;
-  g.n_chunks = c->n_chunks;
   g.ls_cam = c->d_ls_cam;
   g.ls_m = c->d_ls_m;
   g.lm_off = c->d_lm_off;
-  g.task_lm = c->d_task_lm;
+  g.task = reinterpret_cast<const int4*>(c->d_task_lm);
   g.cs_lm = c->d_cs_lm;
   g.cs_m = c->d_cs_m;
-  g.chunk_off = c->d_chunk_off;
-  g.chunk_cam = c->d_chunk_cam;
-  g.cam_chunk = c->d_cam_chunk;
+  g.cs_pos = c->d_cs_pos;
+  g.cam_off = c->d_cam_off;
+  g.ls2cs = c->d_ls2cs;
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -265,6 +262,9 @@ static void alloc_buffers(pv_ctx* c) {
   c->lrec = c->alloc<double>(nl * LREC);
   c->lsys = c->alloc<double>(nl * LSYS);
   c->lvr = c->alloc<double>(nl * 8);
+  c->tarr = c->alloc<double>((size_t)c->n_os * 4);  // t per camera-sorted observation
+  c->cs_x = c->alloc<double>((size_t)c->n_os * 4);
+  c->sbuf = c->alloc<double>((size_t)c->n_os * 4);
   c->lbl = c->alloc<double>(nl * 4);
   c->ldl = c->alloc<double>(nl * 4);
   c->tlm = c->alloc<double>(nl * 4);
@@ -276,9 +276,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->cx = c->alloc<double>(np * 12);
   c->crhs = c->alloc<double>(np * 12);
   c->ch = c->alloc<double>(np * 12);
-  c->cyc = c->alloc<double>((size_t)c->n_chunks * 12);
   c->cyr = c->alloc<double>(np * 12);
-  c->lin_part = c->alloc<double>((size_t)c->n_chunks * LINP);
   c->cUraw = c->alloc<double>(np * LINP);
   c->nrm = c->alloc<double>(np * 2);
   c->cpart = c->alloc<double>((size_t)c->nblk_tasks());
@@ -320,12 +318,10 @@ static void op_cost(pv_ctx* c, int which, double* f) {
 template <int S>
 static int op_linearize(pv_ctx* c) {
   CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
+  k_build_csx<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x);
   k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr, c->lbl,
                                                       c->flags, c->coef);
-  k_lin_cam<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lin_part,
-                                                        c->coef);
-  k_lin_cam_reduce<<<blocks_for(c->n_p * LINP, 256), 256, 0, c->stream>>>(c->g, c->lin_part,
-                                                                         c->cUraw);
+  k_lin_cam<S><<<(int)c->n_p, FT, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->cUraw, c->coef);
   c->launched(3);
   c->check_launch();
   c->allreduce(c->cUraw, (size_t)c->n_p * LINP);
@@ -367,44 +363,49 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   if (n_deg) *n_deg = fl[F_N_DEGEN];
 }
 
-template <int S>
-static void launch_epilogue(pv_ctx* c, int mode, int term, double thr) {
-  auto go = [&](int part) {
-    switch (mode) {
-      case EPI_RHS:
-        k_epilogue<S, EPI_RHS><<<c->nblk_epi(), 256, 0, c->stream>>>(
-            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
-            c->host_ctl_dev, c->ticket, part, term, thr);
-        break;
-      case EPI_TERM:
-        k_epilogue<S, EPI_TERM><<<c->nblk_epi(), 256, 0, c->stream>>>(
-            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
-            c->host_ctl_dev, c->ticket, part, term, thr);
-        break;
-      default:
-        k_epilogue<S, EPI_RAW><<<c->nblk_epi(), 256, 0, c->stream>>>(
-            c->g, c->crec, c->cyc, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch, c->nrm, c->ctl,
-            c->host_ctl_dev, c->ticket, part, term, thr);
+template <int S, int MODE>
+static void launch_cam(pv_ctx* c, int term, double thr) {
+  constexpr bool fused = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM;
+  constexpr bool staged = MODE != CM_PROJECT;
+  Tune tn = c->tune;
+  if (!staged) tn.stage_cap = 0;
+  const int smem = cam_smem_bytes(tn.stage_cap);
+  if (staged) {
+    static bool attr_set = false;  // per template instantiation
+    if (!attr_set) {
+      CK(cudaFuncSetAttribute(k_cam<S, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              cam_smem_bytes(CM_STAGE_MAX)));
+      attr_set = true;
     }
-    c->launched();
-  };
-  if (c->world > 1) {
-    go(EPI_REDUCE_ONLY);
-    c->allreduce(c->cyr, (size_t)c->n_p * 12);
-    go(EPI_APPLY_ONLY);
-  } else {
-    go(EPI_FULL);
   }
+  k_cam<S, MODE><<<(int)c->n_p, FT, smem, c->stream>>>(
+      c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch,
+      c->nrm, c->ctl, c->host_ctl_dev, c->ticket, term, thr, c->coef, tn);
+  c->launched();
 }
 
+template <int S, int MODE>
+static void launch_lm_reduce(pv_ctx* c) {
+  const int nb = blocks_for((long long)((c->n_tasks + LR_BATCH - 1) / LR_BATCH) * 32, 256);
+  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(
+      c->g, c->sbuf, c->lrec, c->tarr, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
+      c->tune);
+  c->launched();
+}
+
+// camera half of a term: y -> epilogue -> next gather (fused on one GPU; split
+// around the NCCL allreduce of y when sharded)
 template <int S>
-static void launch_term(pv_ctx* c, int term, double thr) {
-  k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
-      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
-  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 1,
-                                                       c->coef);
-  c->launched(2);
-  launch_epilogue<S>(c, EPI_TERM, term, thr);
+static void launch_cam_term(pv_ctx* c, bool rhs, int term, double thr) {
+  if (c->world == 1) {
+    if (rhs) launch_cam<S, CM_FUSED_RHS>(c, term, thr);
+    else launch_cam<S, CM_FUSED_TERM>(c, term, thr);
+  } else {
+    launch_cam<S, CM_Y>(c, term, thr);
+    c->allreduce(c->cyr, (size_t)c->n_p * 12);
+    if (rhs) launch_cam<S, CM_EPI_RHS>(c, term, thr);
+    else launch_cam<S, CM_EPI_TERM>(c, term, thr);
+  }
 }
 
 template <int S>
@@ -413,17 +414,14 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
   c->sync();
   std::memset(c->host_ctl, 0, sizeof(PowerCtl));
-  // K4: reduced RHS and t_0 = U^-1 rhs
-  k_lm_rhs_t<S><<<blocks_for(c->n_ls, 256), 256, 0, c->stream>>>(c->n_ls, c->lbl, c->lsys,
-                                                                  c->lrec);
-  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 0,
-                                                       c->coef);
-  c->launched(2);
-  launch_epilogue<S>(c, EPI_RHS, 0, thr);
+  // K4: reduced RHS, t_0 = U^-1 rhs and the gather of term 1
+  launch_lm_reduce<S, LR_RHS>(c);
+  launch_cam_term<S>(c, true, 0, thr);
   c->check_launch();
   // K5 + K6 terms with a one-term lookahead on the device stop flag
   for (int i = 1; i <= max_order; ++i) {
-    launch_term<S>(c, i, thr);
+    launch_lm_reduce<S, LR_TERM>(c);
+    launch_cam_term<S>(c, false, i, thr);
     CK(cudaEventRecord(c->ev[i & 1], c->stream));
     if (i >= 2) {
       CK(cudaEventSynchronize(c->ev[(i - 1) & 1]));
@@ -433,9 +431,9 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   c->check_launch();
   // K7 back-substitution with v = x
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
-  k_phase1<S, P1_BACKSUB><<<c->nblk_tasks(), 256, 0, c->stream>>>(
-      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
-  c->launched(2);
+  c->launched();
+  launch_cam<S, CM_1A>(c, 0, thr);
+  launch_lm_reduce<S, LR_BACKSUB>(c);
   c->check_launch();
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
@@ -560,24 +558,6 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
       std::memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&c->comm, world, id, rank));
     }
-    // factor table of the camera linearization (record offsets, see k_lin_cam)
-    {
-      unsigned char tab[LINP][3];
-      const int symidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-      int e = 0;
-      for (int i = 0; i < 12; ++i)
-        for (int j = i; j < 12; ++j, ++e) {
-          tab[e][0] = (unsigned char)(4 + symidx[i / 4][j / 4]);
-          tab[e][1] = (unsigned char)(i % 4);
-          tab[e][2] = (unsigned char)(j % 4);
-        }
-      for (int kk = 0; kk < 12; ++kk, ++e) {
-        tab[e][0] = (unsigned char)(10 + kk / 4);
-        tab[e][1] = (unsigned char)(kk % 4);
-        tab[e][2] = 13;  // constant 1
-      }
-      CK(cudaMemcpyToSymbol(c_lin_idx, tab, sizeof(tab)));
-    }
     build_graph(c, cam_idx, lm_idx, meas, lm_begin, lm_end);
     alloc_buffers(c);
     c->sync();
@@ -617,12 +597,34 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_NL_LOCAL] = c->n_ls;
   out[PV_INFO_NO_LOCAL] = c->n_os;
   out[PV_INFO_TASKS] = c->n_tasks;
-  out[PV_INFO_CHUNKS] = c->n_chunks;
+  out[PV_INFO_CHUNKS] = c->n_p;
   out[PV_INFO_LAUNCHES] = c->launches;
   out[PV_INFO_RANK] = c->rank;
   out[PV_INFO_WORLD] = c->world;
   out[PV_INFO_DEVICE_BYTES] = (int64_t)c->device_bytes;
   out[PV_INFO_NL_GLOBAL] = c->n_l_global;
+  API_END(c)
+}
+
+int pv_set_option(pv_ctx* c, int key, int64_t value) {
+  API_BEGIN(c)
+  switch (key) {
+    case PV_OPT_STAGE_CAP:
+      if (value < 0 || value > CM_STAGE_MAX) throw PvError(PV_EINVAL, "stage cap out of range");
+      c->tune.stage_cap = (int)value;
+      break;
+    case PV_OPT_POL_STREAM:
+      c->tune.pol_stream = (int)value;
+      break;
+    case PV_OPT_POL_T:
+      c->tune.pol_t = (int)value;
+      break;
+    case PV_OPT_POL_S:
+      c->tune.pol_s = (int)value;
+      break;
+    default:
+      throw PvError(PV_EINVAL, "unknown option");
+  }
   API_END(c)
 }
 
@@ -795,18 +797,19 @@ static void op_schur_apply(pv_ctx* c, const double* v, double* out) {
   CK(cudaMemcpyAsync(c->ctmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->ctmp, c->ch, c->crec);
-  k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
-      c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
-  k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl, 0,
-                                                       c->coef);
-  c->launched(3);
-  launch_epilogue<S>(c, EPI_RAW, 0, 0.0);
+  c->launched();
+  launch_cam<S, CM_1A>(c, 0, 0.0);
+  launch_lm_reduce<S, LR_TERM>(c);
+  launch_cam<S, CM_Y>(c, 0, 0.0);
+  c->allreduce(c->cyr, (size_t)c->n_p * 12);
+  if (S == 2) launch_cam<S, CM_PROJECT>(c, 0, 0.0);
   c->check_launch();
   CK(cudaMemcpyAsync(h.data(), c->cyr, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   for (int64_t i = 0; i < c->n_p; ++i)
     for (int q = 0; q < D; ++q) out[i * D + q] = h[i * 12 + q];
 }
+
 
 extern "C" {
 
@@ -827,14 +830,17 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   float acc[4] = {0, 0, 0, 0};
   for (int i = 1; i <= n; ++i) {
     CK(cudaEventRecord(c->tev[0], c->stream));
-    k_phase1<S, P1_TERM><<<c->nblk_tasks(), 256, 0, c->stream>>>(
-        c->g, c->crec, c->lrec, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags, c->coef);
+    launch_lm_reduce<S, LR_TERM>(c);
     CK(cudaEventRecord(c->tev[1], c->stream));
-    k_phase2<S><<<c->nblk_chunks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->cyc, c->ctl,
-                                                         0, c->coef);
-    CK(cudaEventRecord(c->tev[2], c->stream));
-    c->launched(2);
-    launch_epilogue<S>(c, EPI_TERM, 1 << 20, -1.0);
+    if (c->world == 1) {
+      launch_cam<S, CM_FUSED_TERM>(c, 1 << 20, -1.0);
+      CK(cudaEventRecord(c->tev[2], c->stream));
+    } else {
+      launch_cam<S, CM_Y>(c, 1 << 20, -1.0);
+      CK(cudaEventRecord(c->tev[2], c->stream));
+      c->allreduce(c->cyr, (size_t)c->n_p * 12);
+      launch_cam<S, CM_EPI_TERM>(c, 1 << 20, -1.0);
+    }
     CK(cudaEventRecord(c->tev[3], c->stream));
     CK(cudaEventSynchronize(c->tev[3]));
     float a, b, d;
@@ -848,6 +854,7 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   }
   for (int q = 0; q < 4; ++q) ms[q] = acc[q] / std::max(n, 1);
 }
+
 
 extern "C" {
 

@@ -49,6 +49,50 @@ __device__ __forceinline__ void st4(double* p, double4 v) {
                : "memory");
 }
 
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint): streaming data
+// is marked evict_first so that the reused landmark vectors stay resident.
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 0 normal, 1 evict_first, 2 evict_last
+__device__ __forceinline__ uint64_t pol_sel(int which) {
+  return which == 1 ? pol_first() : (which == 2 ? pol_last() : pol_normal());
+}
+__device__ __forceinline__ double4 ldg4p(const double* p, uint64_t pol) {
+  double4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ldg2p(const double* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldgip(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st4p(double* p, double4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v.x),
+               "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
@@ -136,6 +180,58 @@ __device__ __forceinline__ Gen gen_s2(const double4& P0, const double4& P1, cons
   G.g2 = make_double4(-iz * fma(p0, J0.x, p1 * J1.x), -iz * fma(p0, J0.y, p1 * J1.y),
                       -iz * fma(p0, J0.z, p1 * J1.z), -iz * fma(p0, J0.w, p1 * J1.w));
   return G;
+}
+
+// ---------------------------------------------------------------------------
+// "dot-product form" of the two W applications (never forms G):
+//   W t   : y[4c + a] += sigma_c x_a,  sigma_c = G_c . t from q_r = P_r . t
+//   W^T v : s = sum_r f_r P_r (stage 1: rows restricted to xyz) from d_c = x . v_c
+// stage 1: sigma = (q0 - s m0 q2, q1 - s m1 q2, -s m0 q0 - s m1 q1 + s |m|^2 q2)
+//          f     = (d0 - s m0 d2, d1 - s m1 d2, -s m0 d0 - s m1 d1 + s |m|^2 d2)
+// stage 2: w = iz^2, e_r = q_r - pi_r q2 (resp. d_r - pi_r d2):
+//          sigma = w (e0, e1, -(pi0 e0 + pi1 e1)),  f = w (e0, e1, -(pi0 e0 + pi1 e1))
+
+struct Proj {  // per-observation projection scalars
+  double a0, a1;  // stage 1: s m0, s m1      stage 2: pi0, pi1
+  double c2;      // stage 1: s |m|^2         stage 2: unused
+  double w;       // stage 1: 1               stage 2: iz^2
+};
+
+__device__ __forceinline__ Proj proj_s1(double m0, double m1, double s) {
+  Proj p;
+  p.a0 = s * m0;
+  p.a1 = s * m1;
+  p.c2 = s * fma(m0, m0, m1 * m1);
+  p.w = 1.0;
+  return p;
+}
+
+__device__ __forceinline__ Proj proj_s2(const double4& P0, const double4& P1, const double4& P2,
+                                        const double4& x) {
+  const double u0 = dot4(P0, x), u1 = dot4(P1, x), u2 = dot4(P2, x);
+  const double iz = 1.0 / u2;
+  Proj p;
+  p.a0 = u0 * iz;
+  p.a1 = u1 * iz;
+  p.c2 = 0.0;
+  p.w = iz * iz;
+  return p;
+}
+
+// maps (q0, q1, q2) -> (sigma0, sigma1, sigma2); same map for d -> f
+template <int STAGE>
+__device__ __forceinline__ void proj_map(const Proj& p, double q0, double q1, double q2,
+                                         double& o0, double& o1, double& o2) {
+  if (STAGE == 1) {
+    o0 = fma(-p.a0, q2, q0);
+    o1 = fma(-p.a1, q2, q1);
+    o2 = fma(p.c2, q2, -fma(p.a0, q0, p.a1 * q1));
+  } else {
+    const double e0 = fma(-p.a0, q2, q0), e1 = fma(-p.a1, q2, q1);
+    o0 = p.w * e0;
+    o1 = p.w * e1;
+    o2 = -p.w * fma(p.a0, e0, p.a1 * e1);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,42 +1,56 @@
 // sm_100a kernels of the PoVar / RiPoBA hot path.  See DESIGN.md for the data
 // layout and the roofline of each kernel.  Two traversal orders are used:
 //
+//  * camera-major: one CTA owns one camera and streams that camera's
+//    observations (camera-sorted copies of m and x).  Camera data (P, the term
+//    vector v, U^-1) is CTA-uniform, so it is read once per CTA instead of once
+//    per observation.  Used by the fused power-series term kernel k_cam
+//    (K5 scatter half + K6 epilogue + the next term's K5 gather half) and by
+//    the camera side of the linearization (k_lin_cam).  Per-camera sums are
+//    register accumulations + a fixed-order block reduction: no atomics,
+//    bit-reproducible.
 //  * landmark-major "tasks": one warp owns a run of whole landmarks whose
 //    observations fit in 32 lanes (or one long landmark, looped in 32-obs
-//    slabs).  Used by K1/K2 (k_lin_lm), K5 gather (k_phase1), K7 (back-sub),
-//    K9 (k_cost) and K10 (k_resolve).  Segment sums use a deterministic
-//    shuffle tree.
-//  * camera-major "chunks": one warp owns <= PV_CHUNK consecutive
-//    observations of a single camera (camera-sorted permutation).  Used by
-//    K3 (k_lin_cam) and the K5 scatter half (k_phase2): per-camera sums are
-//    register accumulations + a fixed-order chunk reduction, so no atomics and
-//    bit-reproducible results.
+//    slabs).  Used by the landmark side of the linearization (k_lin_lm), the
+//    per-landmark reduction + V^+ of each term (k_lm_reduce, also K7
+//    back-substitution), the cost (k_cost) and the closed-form landmark
+//    re-solve (k_resolve).  Segment sums use a deterministic shuffle tree.
 #pragma once
 #include "pv_device.cuh"
 
 namespace pv {
 
-constexpr int PV_CHUNK = 256;
 constexpr int CREC = 24;  // camera record: P (12) | v (12)
-constexpr int LREC = 8;   // landmark record: x (4) | t (4)
+constexpr int LREC = 4;   // landmark record: x (4)
 constexpr int LSYS = 8;   // V+ (6) | degenerate (1) | pad
-constexpr int LINP = 90;  // camera linearization partial: U upper (78) | b_p (12)
+constexpr int LINP = 90;  // camera linearization: U upper (78) | b_p (12)
+constexpr int FT = 256;   // threads of a camera CTA
+constexpr int CM_STAGE_MAX = 2048;  // max observations of a camera staged in shared memory
+
+// runtime tuning of the term kernels (pv_set_option): on-chip staging capacity
+// and L2 eviction priorities (0 normal, 1 evict_first, 2 evict_last)
+struct Tune {
+  int stage_cap;   // observations per camera staged in shared memory
+  int pol_stream;  // camera-sorted streams (m, x, ids)
+  int pol_t;       // landmark vectors t (gathered)
+  int pol_s;       // per-observation partials s (scattered / streamed)
+};
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
-       F_COUNT = 8 };
+       F_N_FALLBACK = 5, F_COUNT = 8 };
 
 struct Graph {
   int n_p, n_l, n_o;
-  int n_tasks, n_chunks;
+  int n_tasks;
   const int* ls_cam;     // [n_o] camera of each landmark-sorted observation
   const double* ls_m;    // [n_o*2]
   const int* lm_off;     // [n_l+1]
-  const int* task_lm;    // [n_tasks+1]
+  const int4* task;      // [n_tasks] {o0, n, l0, segment-head mask}
   const int* cs_lm;      // [n_o] local landmark of each camera-sorted observation
+  const int* cs_pos;     // [n_o] landmark-sorted position of each camera-sorted observation
+  const int* ls2cs;      // [n_o] camera-sorted position of each landmark-sorted observation
   const double* cs_m;    // [n_o*2]
-  const int* chunk_off;  // [n_chunks+1]
-  const int* chunk_cam;  // [n_chunks]
-  const int* cam_chunk;  // [n_p+1]
+  const int* cam_off;    // [n_p+1] camera-sorted offsets
 };
 
 struct PowerCtl {
@@ -58,21 +72,19 @@ struct Coef {
 // landmark task decoding
 
 struct Task {
-  int l0, l1, o0, n;
+  int l0, o0, n;
   bool long_task;
   unsigned heads;
 };
 
 __device__ __forceinline__ Task load_task(const Graph& g, int w, int lane) {
+  const int4 d = __ldg(g.task + w);
   Task t;
-  t.l0 = g.task_lm[w];
-  t.l1 = g.task_lm[w + 1];
-  t.o0 = g.lm_off[t.l0];
-  t.n = g.lm_off[t.l1] - t.o0;
-  t.long_task = (t.l1 - t.l0 == 1) && t.n > 32;
-  unsigned bit = 0;
-  if (!t.long_task && lane < t.l1 - t.l0) bit = 1u << (g.lm_off[t.l0 + lane] - t.o0);
-  t.heads = t.long_task ? 1u : __reduce_or_sync(PV_FULL, bit);
+  t.o0 = d.x;
+  t.n = d.y;
+  t.l0 = d.z;
+  t.heads = (unsigned)d.w;
+  t.long_task = t.n > 32;
   return t;
 }
 
@@ -95,247 +107,221 @@ __device__ __forceinline__ int seg_start_lane(const Task& t, int lane) {
 }
 
 // ---------------------------------------------------------------------------
-// K5 gather half / K7: landmark-major  W^T v  (+ V+ and the landmark epilogue)
+// camera-major fused power-series term (K5 scatter + K6 epilogue + K5 gather)
+//
+//   phase 2 : y_i   = sum_{j in cam i} W_ij t_j           (t gathered per obs)
+//   epilogue: t_i   = U_i^-1 (rhs_i | y_i), x_i += t_i, v_i = t_i (B t_i)
+//   phase 1a: s_ij  = W_ij^T v_i  -> sbuf[landmark-sorted position]
+//
+// The landmark half (t_j = V_j^+ sum_i s_ij) is k_lm_reduce.
 
-enum { P1_TERM = 0, P1_BACKSUB = 1 };
-
-template <int STAGE>
-__device__ __forceinline__ void wtv_obs(const double* __restrict__ crec, int cam, double m0,
-                                        double m1, const double4& x, const Coef& k,
-                                        double (&acc)[4]) {
-  const double* c = crec + (size_t)cam * CREC;
-  double4 P0 = ldg4(c), P1 = ldg4(c + 4), P2 = ldg4(c + 8);
-  double4 v0 = ldg4(c + 12), v1 = ldg4(c + 16), v2 = ldg4(c + 20);
-  Gen G = STAGE == 1 ? gen_s1(P0, P1, P2, m0, m1, k.s) : gen_s2(P0, P1, P2, x);
-  double d0 = dot4(x, v0), d1 = dot4(x, v1), d2 = dot4(x, v2);
-  acc[0] = fma(d0, G.g0.x, fma(d1, G.g1.x, fma(d2, G.g2.x, acc[0])));
-  acc[1] = fma(d0, G.g0.y, fma(d1, G.g1.y, fma(d2, G.g2.y, acc[1])));
-  acc[2] = fma(d0, G.g0.z, fma(d1, G.g1.z, fma(d2, G.g2.z, acc[2])));
-  if (STAGE == 2) acc[3] = fma(d0, G.g0.w, fma(d1, G.g1.w, fma(d2, G.g2.w, acc[3])));
-}
-
-template <int STAGE, int MODE>
-__device__ __forceinline__ void phase1_finish(int l, const double (&acc)[4], const double4& x,
-                                              double* __restrict__ lrec,
-                                              const double* __restrict__ lsys,
-                                              const double* __restrict__ lbl,
-                                              double* __restrict__ ldl, double* __restrict__ tlm,
-                                              int* __restrict__ flags) {
-  double s3[3], h[4];
-  double xv[4] = {x.x, x.y, x.z, x.w};
-  if (STAGE == 1) {
-    s3[0] = acc[0];
-    s3[1] = acc[1];
-    s3[2] = acc[2];
-  } else {
-    householder_h<4>(xv, h);
-    basis_apply_t<4>(h, acc, s3);
-  }
-  const double* vs = lsys + (size_t)l * LSYS;
-  double vp[6] = {vs[0], vs[1], vs[2], vs[3], vs[4], vs[5]};
-  if (MODE == P1_TERM) {
-    double t[3];
-    sym3_apply(vp, s3, t);
-    if (STAGE == 1) {
-      st4(lrec + (size_t)l * LREC + 4, make_double4(t[0], t[1], t[2], 0.0));
-    } else {
-      double t4[4];
-      basis_apply<4>(h, t, t4);
-      st4(lrec + (size_t)l * LREC + 4, make_double4(t4[0], t4[1], t4[2], t4[3]));
-    }
-  } else {
-    const double* bl = lbl + (size_t)l * 4;
-    double q[3] = {s3[0] + bl[0], s3[1] + bl[1], s3[2] + bl[2]};
-    double dl[3];
-    sym3_apply(vp, q, dl);
-    bool degen = vs[6] != 0.0;
-    for (int i = 0; i < 3; ++i) dl[i] = degen ? 0.0 : -dl[i];
-    st4(ldl + (size_t)l * 4, make_double4(dl[0], dl[1], dl[2], 0.0));
-    if (STAGE == 1) {
-      st4(tlm + (size_t)l * 4, make_double4(x.x + dl[0], x.y + dl[1], x.z + dl[2], x.w));
-    } else {
-      double b[4];
-      basis_apply<4>(h, dl, b);
-      double y0 = x.x + b[0], y1 = x.y + b[1], y2 = x.z + b[2], y3 = x.w + b[3];
-      double nn = sqrt(y0 * y0 + y1 * y1 + y2 * y2 + y3 * y3);
-      if (nn == 0.0) {
-        atomicOr(flags + F_ZERO_NORM, 1);
-        nn = 1.0;
-      }
-      st4(tlm + (size_t)l * 4, make_double4(y0 / nn, y1 / nn, y2 / nn, y3 / nn));
-    }
-  }
-}
-
-template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_phase1(Graph g, const double* __restrict__ crec,
-                                                double* __restrict__ lrec,
-                                                const double* __restrict__ lsys,
-                                                const double* __restrict__ lbl,
-                                                double* __restrict__ ldl, double* __restrict__ tlm,
-                                                const PowerCtl* __restrict__ ctl, int* flags,
-                                                Coef k) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= g.n_tasks) return;
-  if (MODE == P1_TERM && ctl->stopped) return;
-  Task t = load_task(g, w, lane);
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (t.long_task) {
-    double4 x = ldg4(lrec + (size_t)t.l0 * LREC);
-    for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-      double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      wtv_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, k, acc);
-    }
-    warp_reduce_all(acc);
-    if (lane == 0) phase1_finish<STAGE, MODE>(t.l0, acc, x, lrec, lsys, lbl, ldl, tlm, flags);
-  } else {
-    int l, seg_end;
-    lane_segment(t, lane, l, seg_end);
-    double4 x = ldg4(lrec + (size_t)l * LREC);
-    if (lane < t.n) {
-      int o = t.o0 + lane;
-      double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      wtv_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, k, acc);
-    }
-    seg_reduce(acc, lane, seg_end);
-    if (lane < t.n && ((t.heads >> lane) & 1u))
-      phase1_finish<STAGE, MODE>(l, acc, x, lrec, lsys, lbl, ldl, tlm, flags);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K5 scatter half: camera-major  y_chunk = sum_j W_ij t_j
+enum {
+  CM_FUSED_RHS = 0,   // t_rhs -> rhs -> t_0 -> s (term 1)
+  CM_FUSED_TERM = 1,  // t -> y -> t_i -> s (term i+1)
+  CM_Y = 2,           // t -> y (raw 12) -> cyr            (sharded part A, also schur_apply)
+  CM_EPI_RHS = 3,     // cyr -> rhs -> t_0 -> s            (sharded part B)
+  CM_EPI_TERM = 4,    // cyr -> t_i -> s                   (sharded part B)
+  CM_1A = 5,          // crec.v -> s                       (back-substitution, schur_apply)
+  CM_PROJECT = 6      // cyr (raw 12) -> projected (11) in place (schur_apply, stage 2)
+};
 
 template <int STAGE>
-__global__ void __launch_bounds__(256) k_phase2(Graph g, const double* __restrict__ crec,
-                                                const double* __restrict__ lrec,
-                                                double* __restrict__ cyc,
-                                                const PowerCtl* __restrict__ ctl, int check_stop,
-                                                Coef k) {
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= g.n_chunks) return;
-  if (check_stop && ctl->stopped) return;
-  const int cam = __ldg(g.chunk_cam + c);
-  const int o0 = __ldg(g.chunk_off + c), o1 = __ldg(g.chunk_off + c + 1);
-  const double* cp = crec + (size_t)cam * CREC;
-  const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2 = ldg4(cp + 8);
-  double acc[12];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) acc[i] = 0.0;
-#pragma unroll 2
-  for (int o = o0 + lane; o < o1; o += 32) {
-    const int j = __ldg(g.cs_lm + o);
-    const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
-    const double* lr = lrec + (size_t)j * LREC;
-    const double4 X = ldg4(lr), T = ldg4(lr + 4);
-    Gen G = STAGE == 1 ? gen_s1(P0, P1, P2, m.x, m.y, k.s) : gen_s2(P0, P1, P2, X);
-    const double sg[3] = {dot4(G.g0, T), dot4(G.g1, T), dot4(G.g2, T)};
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      acc[4 * q + 0] = fma(sg[q], X.x, acc[4 * q + 0]);
-      acc[4 * q + 1] = fma(sg[q], X.y, acc[4 * q + 1]);
-      acc[4 * q + 2] = fma(sg[q], X.z, acc[4 * q + 2]);
-      acc[4 * q + 3] = fma(sg[q], X.w, acc[4 * q + 3]);
-    }
-  }
+__device__ __forceinline__ Gen obs_gen(const double4& P0, const double4& P1, const double4& P2,
+                                       const double2& m, const double4& X, const Coef& k) {
+  return STAGE == 1 ? gen_s1(P0, P1, P2, m.x, m.y, k.s) : gen_s2(P0, P1, P2, X);
+}
+
+__device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT/32*12]*/,
+                                            double* out /*[12]*/) {
   warp_reduce_all(acc);
-  double mine = 0.0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
 #pragma unroll
-  for (int i = 0; i < 12; ++i)
-    if (lane == i) mine = acc[i];
-  if (lane < 12) cyc[(size_t)c * 12 + lane] = mine;
+    for (int i = 0; i < 12; ++i) red[w * 12 + i] = acc[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 12) {
+    double s = 0.0;
+    for (int q = 0; q < FT / 32; ++q) s += red[q * 12 + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// K4/K6 epilogue: per camera (half-warp), reduce chunk partials, U^-1, series
-// accumulation, stop test (last block), next term's camera vector.
-
-enum { EPI_RHS = 0, EPI_TERM = 1, EPI_RAW = 2 };
-enum { EPI_FULL = 0, EPI_REDUCE_ONLY = 1, EPI_APPLY_ONLY = 2 };
-
-__device__ __forceinline__ double hw_sum(double v) {
-#pragma unroll
-  for (int d = 8; d > 0; d >>= 1) v += __shfl_xor_sync(PV_FULL, v, d, 16);
-  return v;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// dynamic shared memory of a camera CTA staging `cap` observations (x, m)
+__host__ __device__ constexpr int cam_smem_bytes(int cap) { return cap * (32 + 16); }
+
+constexpr int CM_BATCH = 4;  // independent t gathers in flight per thread
 
 template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_epilogue(
-    Graph g, double* __restrict__ crec, const double* __restrict__ cyc, double* __restrict__ cyr,
+__global__ void __launch_bounds__(FT, 2) k_cam(
+    Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
+    const double* __restrict__ tbuf, double* __restrict__ sbuf, double* __restrict__ cyr,
     const double* __restrict__ cbp, const double* __restrict__ cUi, double* __restrict__ cx,
     double* __restrict__ crhs, const double* __restrict__ ch, double* __restrict__ nrm,
     PowerCtl* __restrict__ ctl, volatile PowerCtl* host_ctl, unsigned* __restrict__ ticket,
-    int part, int term, double thr) {
-  __shared__ double red[2][256];
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31;
-  const int r = lane & 15;
-  const int cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-  if (MODE == EPI_TERM && ctl->stopped) return;  // uniform over the grid
-  const bool valid = cam < g.n_p;
+    int term, double thr, Coef k, Tune tune) {
+  constexpr bool P2 = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM || MODE == CM_Y;
+  constexpr bool FROM_CYR = MODE == CM_EPI_RHS || MODE == CM_EPI_TERM;
+  constexpr bool EPI = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM || FROM_CYR;
+  constexpr bool RHS = MODE == CM_FUSED_RHS || MODE == CM_EPI_RHS;
+  constexpr bool A1 = EPI || MODE == CM_1A;
   constexpr int D = STAGE == 1 ? 12 : 11;
-  double u = 0.0;
-  if (valid && r < 12) {
-    if (part == EPI_APPLY_ONLY) {
-      u = cyr[(size_t)cam * 12 + r];
-    } else {
-      const int c0 = g.cam_chunk[cam], c1 = g.cam_chunk[cam + 1];
-      for (int c = c0; c < c1; ++c) u += cyc[(size_t)c * 12 + r];
+  __shared__ double red[(FT / 32) * 12];
+  __shared__ double ysm[12];
+  __shared__ double vsm[12];
+  __shared__ bool last;
+  extern __shared__ __align__(32) unsigned char dsm[];
+  const int cap = tune.stage_cap;
+  double4* sx = reinterpret_cast<double4*>(dsm);
+  double2* smm = reinterpret_cast<double2*>(dsm + (size_t)cap * 32);
+  const int cam = blockIdx.x;
+  if ((MODE == CM_FUSED_TERM || MODE == CM_EPI_TERM) && ctl->stopped) return;  // grid-uniform
+  const int tid = threadIdx.x;
+  const int o0 = g.cam_off[cam], o1 = g.cam_off[cam + 1];
+  const int n = o1 - o0;
+  const double* cp = crec + (size_t)cam * CREC;
+  const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2v = ldg4(cp + 8);
+  const uint64_t pf = pol_sel(tune.pol_stream), pl = pol_sel(tune.pol_t),
+                 ps = pol_sel(tune.pol_s);
+
+  if (MODE == CM_PROJECT) {  // stage-2 tangent projection of a raw y, in place
+    if (tid < 32) {
+      const int r = tid & 15;
+      double u = (tid < 12) ? cyr[(size_t)cam * 12 + tid] : 0.0;
+      double h = (tid < 12) ? ch[(size_t)cam * 12 + tid] : 0.0;
+      double hu = warp_sum(tid < 16 ? h * u : 0.0);
+      double pr = u - 2.0 * h * hu;
+      double nx = __shfl_sync(PV_FULL, pr, (r + 1) & 31);
+      if (tid < 12) cyr[(size_t)cam * 12 + tid] = tid < 11 ? nx : 0.0;
+    }
+    return;
+  }
+
+  // ---- stage this camera's x and m in shared memory for the second (gather) half
+  const int nc = A1 && P2 ? min(n, cap) : 0;
+  if (nc > 0) {
+    const char* gx = reinterpret_cast<const char*>(cs_x + 4 * (size_t)o0);
+    for (int q = tid; q < 2 * nc; q += FT) cp_async16(dsm + 16 * (size_t)q, gx + 16 * (size_t)q);
+    const char* gm = reinterpret_cast<const char*>(g.cs_m + 2 * (size_t)o0);
+    for (int q = tid; q < nc; q += FT) cp_async16(smm + q, gm + 16 * (size_t)q);
+  }
+
+  if (P2) {  // y_i = sum_j W_ij t_j, t streamed per observation (camera-sorted)
+    double acc[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+#pragma unroll 4
+    for (int q = tid; q < n; q += FT) {
+      const size_t o = (size_t)(o0 + q);
+      const double4 T = ldg4p(tbuf + 4 * o, pl);
+      const double4 X = ldg4p(cs_x + 4 * o, pf);
+      const double2 m = ldg2p(g.cs_m + 2 * o, pf);
+      const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
+      double sg[3];
+      proj_map<STAGE>(pj, dot4(P0, T), dot4(P1, T), dot4(P2v, T), sg[0], sg[1], sg[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc[4 * c + 0] = fma(sg[c], X.x, acc[4 * c + 0]);
+        acc[4 * c + 1] = fma(sg[c], X.y, acc[4 * c + 1]);
+        acc[4 * c + 2] = fma(sg[c], X.z, acc[4 * c + 2]);
+        acc[4 * c + 3] = fma(sg[c], X.w, acc[4 * c + 3]);
+      }
+    }
+    cp_async_wait_all();
+    block_sum12(acc, red, ysm);
+    if (MODE == CM_Y) {
+      if (tid < 12) cyr[(size_t)cam * 12 + tid] = ysm[tid];
+      return;
     }
   }
-  if (part == EPI_REDUCE_ONLY) {
-    if (valid && r < 12) cyr[(size_t)cam * 12 + r] = u;
-    return;
-  }
-  double h = 0.0;
-  if (STAGE == 2) {  // project y (12) -> tangent (11)
-    h = (valid && r < 12) ? ch[(size_t)cam * 12 + r] : 0.0;
-    double hu = hw_sum(h * u);
-    double proj = u - 2.0 * h * hu;  // component r of H y
-    u = __shfl_sync(PV_FULL, proj, (r + 1) & 15, 16);
-    if (r >= 11) u = 0.0;
-  }
-  if (MODE == EPI_RAW) {
-    if (valid && r < 12) cyr[(size_t)cam * 12 + r] = u;
-    return;
-  }
-  double vin = u;
-  if (MODE == EPI_RHS) {
-    double b = (valid && r < D) ? cbp[(size_t)cam * 12 + r] : 0.0;
-    vin = (r < D) ? -(b - u) : 0.0;
-    if (valid && r < 12) crhs[(size_t)cam * 12 + r] = vin;
-  }
-  double t = 0.0;
-  const double* Ui = cUi + (size_t)cam * 144 + r * 12;
+
+  if (EPI) {
+    if (tid < 32) {  // warp 0: rows r < D of U^-1
+      const int r = tid & 15;
+      const bool row = tid < 12;
+      double u = 0.0;
+      if (row) u = FROM_CYR ? cyr[(size_t)cam * 12 + tid] : ysm[tid];
+      double h = 0.0;
+      if (STAGE == 2) {  // project y (12) -> tangent (11)
+        h = row ? ch[(size_t)cam * 12 + tid] : 0.0;
+        double hu = warp_sum(tid < 16 ? h * u : 0.0);
+        double pr = u - 2.0 * h * hu;
+        u = __shfl_sync(PV_FULL, pr, (r + 1) & 31);
+        if (tid >= 11) u = 0.0;
+      }
+      double vin = u;
+      if (RHS) {
+        double b = tid < D ? cbp[(size_t)cam * 12 + tid] : 0.0;
+        vin = tid < D ? -(b - u) : 0.0;
+        if (row) crhs[(size_t)cam * 12 + tid] = vin;
+      }
+      double t = 0.0;
+      const double* Ui = cUi + (size_t)cam * 144 + (tid < D ? tid : 0) * 12;
 #pragma unroll
-  for (int kk = 0; kk < 12; ++kk) {
-    double vk = __shfl_sync(PV_FULL, vin, kk, 16);
-    if (valid && r < D && kk < D) t = fma(Ui[kk], vk, t);
+      for (int kk = 0; kk < 12; ++kk) {
+        double vk = __shfl_sync(PV_FULL, vin, kk);
+        if (tid < D && kk < D) t = fma(Ui[kk], vk, t);
+      }
+      double xr = 0.0;
+      if (tid < D) {
+        xr = RHS ? t : cx[(size_t)cam * 12 + tid] + t;
+        cx[(size_t)cam * 12 + tid] = xr;
+      }
+      double v = t;
+      if (STAGE == 2) {  // v = B t (11 -> 12)
+        double tprev = __shfl_sync(PV_FULL, t, (tid + 31) & 31);
+        double e = (tid >= 1 && tid < 12) ? tprev : 0.0;
+        double hd = warp_sum(h * e);
+        v = e - 2.0 * h * hd;
+      }
+      if (row) vsm[tid] = v;
+      double tn = warp_sum(tid < D ? t * t : 0.0);
+      double xn = warp_sum(tid < D ? xr * xr : 0.0);
+      if (tid == 0) {
+        nrm[2 * (size_t)cam] = tn;
+        nrm[2 * (size_t)cam + 1] = xn;
+      }
+    }
+    __syncthreads();
+  } else if (MODE == CM_1A) {
+    if (tid < 12) vsm[tid] = cp[12 + tid];
+    __syncthreads();
   }
-  double xr = 0.0;
-  if (valid && r < D) {
-    xr = MODE == EPI_RHS ? t : cx[(size_t)cam * 12 + r] + t;
-    cx[(size_t)cam * 12 + r] = xr;
+
+  if (A1) {  // phase 1a: s_ij = W_ij^T v_i scattered to landmark-sorted positions
+    const double4 v0 = make_double4(vsm[0], vsm[1], vsm[2], vsm[3]);
+    const double4 v1 = make_double4(vsm[4], vsm[5], vsm[6], vsm[7]);
+    const double4 v2 = make_double4(vsm[8], vsm[9], vsm[10], vsm[11]);
+#pragma unroll 2
+    for (int q = tid; q < n; q += FT) {
+      const int o = o0 + q;
+      const int pos = ldgip(g.cs_pos + o, pf);
+      const double4 X = q < nc ? sx[q] : ldg4p(cs_x + 4 * (size_t)o, pf);
+      const double2 m = q < nc ? smm[q] : ldg2p(g.cs_m + 2 * (size_t)o, pf);
+      const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
+      double f0, f1, f2;
+      proj_map<STAGE>(pj, dot4(X, v0), dot4(X, v1), dot4(X, v2), f0, f1, f2);
+      double4 sv;
+      sv.x = fma(f0, P0.x, fma(f1, P1.x, f2 * P2v.x));
+      sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
+      sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
+      sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
+      st4p(sbuf + 4 * (size_t)pos, sv, ps);
+    }
   }
-  double v = t;
-  if (STAGE == 2) {  // camera vector for the next gather: B t (11 -> 12)
-    double tprev = __shfl_sync(PV_FULL, t, (r + 15) & 15, 16);  // t_{r-1}
-    double e = (r >= 1 && r < 12) ? tprev : 0.0;
-    double hd = hw_sum(h * e);
-    v = e - 2.0 * h * hd;
-  }
-  if (valid && r < 12) crec[(size_t)cam * CREC + 12 + r] = v;
-  double tn = hw_sum(r < D ? t * t : 0.0);
-  double xn = hw_sum(r < D ? xr * xr : 0.0);
-  if (valid && r == 0) {
-    nrm[2 * (size_t)cam] = tn;
-    nrm[2 * (size_t)cam + 1] = xn;
-  }
-  // ---- grid-wide fixed-order norm reduction in the last block
-  __syncthreads();
-  if (threadIdx.x == 0) {
+
+  if (!EPI) return;
+  // ---- grid-wide fixed-order norm reduction + stop test in the last CTA
+  if (tid == 0) {
     __threadfence();
     unsigned tk = atomicAdd(ticket, 1u);
     last = tk == gridDim.x - 1;
@@ -344,30 +330,33 @@ __global__ void __launch_bounds__(256) k_epilogue(
   if (!last) return;
   __threadfence();
   double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < g.n_p; i += blockDim.x) {
+  for (int i = tid; i < g.n_p; i += FT) {
     a += __ldcg(nrm + 2 * (size_t)i);
     b += __ldcg(nrm + 2 * (size_t)i + 1);
   }
-  red[0][threadIdx.x] = a;
-  red[1][threadIdx.x] = b;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      red[0][threadIdx.x] += red[0][threadIdx.x + s];
-      red[1][threadIdx.x] += red[1][threadIdx.x + s];
-    }
-    __syncthreads();
+  double ra[2] = {a, b};
+  warp_reduce_all(ra);
+  __shared__ double rr[2][FT / 32];
+  if ((tid & 31) == 0) {
+    rr[0][tid >> 5] = ra[0];
+    rr[1][tid >> 5] = ra[1];
   }
-  if (threadIdx.x == 0) {
-    double TN = sqrt(red[0][0]), XN = sqrt(red[1][0]);
+  __syncthreads();
+  if (tid == 0) {
+    double TN2 = 0.0, XN2 = 0.0;
+    for (int q = 0; q < FT / 32; ++q) {
+      TN2 += rr[0][q];
+      XN2 += rr[1][q];
+    }
+    const double TN = sqrt(TN2), XN = sqrt(XN2);
     PowerCtl c = *ctl;
-    if (MODE == EPI_RHS) {  // solvers.py:134-139
+    if (RHS) {  // solvers.py:134-139
       c.stopped = 0;
       c.order = 0;
       c.term = 0;
       c.trunc = XN > 0.0 ? 1.0 : 0.0;
     } else {  // solvers.py:140-149
-      double ratio = XN > 0.0 ? TN / XN : 0.0;
+      const double ratio = XN > 0.0 ? TN / XN : 0.0;
       c.trunc = ratio;
       c.term = term;
       if (ratio <= thr) {
@@ -389,6 +378,178 @@ __global__ void __launch_bounds__(256) k_epilogue(
     __threadfence_system();
     *ticket = 0u;
   }
+}
+
+// ---------------------------------------------------------------------------
+// landmark half of a term (and K7): t_j = V_j^+ sum_i s_ij, or the
+// back-substitution dl_j = -V_j^+ (b_l + sum_i s_ij) with the trial landmark.
+
+enum { LR_TERM = 0, LR_BACKSUB = 1, LR_RHS = 2 };
+
+struct LmPre {  // per-landmark inputs of the landmark epilogue, prefetched before the reduce
+  double4 va, vb, bl, x;
+};
+
+template <int STAGE, int MODE>
+__device__ __forceinline__ LmPre lm_prefetch(int l, const double* __restrict__ lrec,
+                                             const double* __restrict__ lsys,
+                                             const double* __restrict__ lbl) {
+  LmPre p;
+  p.va = ldg4(lsys + (size_t)l * LSYS);
+  p.vb = ldg4(lsys + (size_t)l * LSYS + 4);
+  p.x = (STAGE == 2 || MODE == LR_BACKSUB) ? ldg4(lrec + (size_t)l * LREC)
+                                           : make_double4(0.0, 0.0, 0.0, 1.0);
+  p.bl = MODE != LR_TERM ? ldg4(lbl + (size_t)l * 4) : make_double4(0.0, 0.0, 0.0, 0.0);
+  return p;
+}
+
+// landmark epilogue: returns t (lifted to 4 components) for TERM / RHS; writes
+// the landmark update and trial landmark for BACKSUB
+template <int STAGE, int MODE>
+__device__ __forceinline__ double4 lm_finish(int l, const double (&acc)[4], const LmPre& p,
+                                             double* __restrict__ ldl, double* __restrict__ tlm,
+                                             int* __restrict__ flags) {
+  double s3[3], h[4];
+  const double4 x = p.x;
+  double xv[4] = {x.x, x.y, x.z, x.w};
+  if (STAGE == 2) householder_h<4>(xv, h);
+  if (MODE == LR_RHS) {
+    s3[0] = p.bl.x;
+    s3[1] = p.bl.y;
+    s3[2] = p.bl.z;
+  } else if (STAGE == 1) {
+    s3[0] = acc[0];
+    s3[1] = acc[1];
+    s3[2] = acc[2];
+  } else {
+    basis_apply_t<4>(h, acc, s3);
+  }
+  const double vp[6] = {p.va.x, p.va.y, p.va.z, p.va.w, p.vb.x, p.vb.y};
+  if (MODE != LR_BACKSUB) {
+    double t[3];
+    sym3_apply(vp, s3, t);
+    if (STAGE == 1) return make_double4(t[0], t[1], t[2], 0.0);
+    double t4[4];
+    basis_apply<4>(h, t, t4);
+    return make_double4(t4[0], t4[1], t4[2], t4[3]);
+  }
+  double q[3] = {s3[0] + p.bl.x, s3[1] + p.bl.y, s3[2] + p.bl.z};
+  double dl[3];
+  sym3_apply(vp, q, dl);
+  const bool degen = p.vb.z != 0.0;
+  for (int i = 0; i < 3; ++i) dl[i] = degen ? 0.0 : -dl[i];
+  st4(ldl + (size_t)l * 4, make_double4(dl[0], dl[1], dl[2], 0.0));
+  if (STAGE == 1) {
+    st4(tlm + (size_t)l * 4, make_double4(x.x + dl[0], x.y + dl[1], x.z + dl[2], x.w));
+  } else {
+    double b[4];
+    basis_apply<4>(h, dl, b);
+    double y0 = x.x + b[0], y1 = x.y + b[1], y2 = x.z + b[2], y3 = x.w + b[3];
+    double nn = sqrt(y0 * y0 + y1 * y1 + y2 * y2 + y3 * y3);
+    if (nn == 0.0) {
+      atomicOr(flags + F_ZERO_NORM, 1);
+      nn = 1.0;
+    }
+    st4(tlm + (size_t)l * 4, make_double4(y0 / nn, y1 / nn, y2 / nn, y3 / nn));
+  }
+  return make_double4(0.0, 0.0, 0.0, 0.0);
+}
+
+constexpr int LR_BATCH = 4;  // landmark tasks per warp (loads of all of them in flight)
+
+// Landmark half of a term: t_j = V_j^+ sum_i s_ij (TERM) or V_j^+ b_j (RHS), scattered
+// into the camera-sorted slot of every observation of landmark j (tbuf), so that
+// the camera kernel streams it; BACKSUB writes dl_j and the trial landmark instead.
+template <int STAGE, int MODE>
+__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, const double* __restrict__ sbuf,
+                                                   const double* __restrict__ lrec,
+                                                   double* __restrict__ tbuf,
+                                                   const double* __restrict__ lsys,
+                                                   const double* __restrict__ lbl,
+                                                   double* __restrict__ ldl,
+                                                   double* __restrict__ tlm,
+                                                   const PowerCtl* __restrict__ ctl, int* flags,
+                                                   Tune tune) {
+  constexpr bool SCATTER = MODE != LR_BACKSUB;
+  const int lane = threadIdx.x & 31;
+  const int w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LR_BATCH;
+  if (w0 >= g.n_tasks) return;
+  if (MODE == LR_TERM && ctl->stopped) return;
+  const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
+  const int nb = min(LR_BATCH, g.n_tasks - w0);
+  int4 d = make_int4(0, 0, 0, 0);
+  if (lane < nb) d = __ldg(g.task + w0 + lane);
+  Task tk[LR_BATCH];
+  double4 sv[LR_BATCH];
+  int dst[LR_BATCH];
+#pragma unroll
+  for (int q = 0; q < LR_BATCH; ++q) {
+    tk[q].o0 = __shfl_sync(PV_FULL, d.x, q);
+    tk[q].n = __shfl_sync(PV_FULL, d.y, q);
+    tk[q].l0 = __shfl_sync(PV_FULL, d.z, q);
+    tk[q].heads = (unsigned)__shfl_sync(PV_FULL, d.w, q);
+    tk[q].long_task = tk[q].n > 32;
+    sv[q] = make_double4(0.0, 0.0, 0.0, 0.0);
+    dst[q] = 0;
+    if (q < nb && !tk[q].long_task && lane < tk[q].n) {
+      if (MODE != LR_RHS) sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
+      if (SCATTER) dst[q] = ldgip(g.ls2cs + tk[q].o0 + lane, pf);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < LR_BATCH; ++q) {
+    if (q >= nb) break;
+    const Task& t = tk[q];
+    if (t.long_task) {
+      const LmPre pre = lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (MODE != LR_RHS) {
+        for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
+          const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
+          acc[0] += s.x;
+          acc[1] += s.y;
+          acc[2] += s.z;
+          acc[3] += s.w;
+        }
+        warp_reduce_all(acc);
+      }
+      double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (lane == 0) tv = lm_finish<STAGE, MODE>(t.l0, acc, pre, ldl, tlm, flags);
+      if (SCATTER) {
+        tv.x = __shfl_sync(PV_FULL, tv.x, 0);
+        tv.y = __shfl_sync(PV_FULL, tv.y, 0);
+        tv.z = __shfl_sync(PV_FULL, tv.z, 0);
+        tv.w = __shfl_sync(PV_FULL, tv.w, 0);
+        for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32)
+          st4p(tbuf + 4 * (size_t)ldgip(g.ls2cs + o, pf), tv, pt);
+      }
+    } else {
+      int l, seg_end;
+      lane_segment(t, lane, l, seg_end);
+      const bool head = lane < t.n && ((t.heads >> lane) & 1u);
+      LmPre pre;
+      if (head) pre = lm_prefetch<STAGE, MODE>(l, lrec, lsys, lbl);
+      double acc[4] = {sv[q].x, sv[q].y, sv[q].z, sv[q].w};
+      if (MODE != LR_RHS) seg_reduce(acc, lane, seg_end);
+      double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (head) tv = lm_finish<STAGE, MODE>(l, acc, pre, ldl, tlm, flags);
+      if (SCATTER) {
+        const int src = seg_start_lane(t, lane < t.n ? lane : 0);
+        tv.x = __shfl_sync(PV_FULL, tv.x, src);
+        tv.y = __shfl_sync(PV_FULL, tv.y, src);
+        tv.z = __shfl_sync(PV_FULL, tv.z, src);
+        tv.w = __shfl_sync(PV_FULL, tv.w, src);
+        if (lane < t.n) st4p(tbuf + 4 * (size_t)dst[q], tv, pt);
+      }
+    }
+  }
+}
+
+// camera-sorted copy of the landmark coordinates (once per linearization point)
+__global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __restrict__ cs_x) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= g.n_o) return;
+  st4(cs_x + 4 * (size_t)o, ldg4(lrec + (size_t)__ldg(g.cs_lm + o) * LREC));
 }
 
 // ---------------------------------------------------------------------------
@@ -519,109 +680,131 @@ __global__ void __launch_bounds__(256) k_lin_lm(Graph g, const double* __restric
 }
 
 // ---------------------------------------------------------------------------
-// K3 (camera side of the linearization): U = sum (A (x) x x^T), b_p = sum h (x) x
-// U[4c+a][4d+b] = sum A_cd x_a x_b,  b_p[4c+a] = sum h_c x_a.
-
-__constant__ unsigned char c_lin_idx[LINP][3];  // record offsets of the three factors
+// K3 camera side of the linearization, camera-major (one CTA per camera).
+// U = sum_obs A(w) (x) x x^T with A = [[c00 w0, 0, c02 w1], [0, c00 w0, c12 w2],
+// [c02 w1, c12 w2, c22 w3]] and b_p = sum_obs h (x) x:
+//   stage 1: w = (1, m0, m1, |m|^2),  (c00, c02, c12, c22) = (s1^2+s2^2, -s1^2, -s1^2, s1^2)
+//            h = K^T r  (objective.py:95-110 rows)
+//   stage 2: w = iz^2 (1, pi0, pi1, |pi|^2), (c00, c02, c12, c22) = (1, -1, -1, 1)
+//            h = dpi^T r (objective.py:128-146)
+// Output: 78 upper entries of U (row-major i <= j) + 12 of b_p per camera.
 
 template <int STAGE>
-__global__ void __launch_bounds__(256) k_lin_cam(Graph g, const double* __restrict__ crec,
-                                                 const double* __restrict__ lrec,
-                                                 double* __restrict__ part, Coef k) {
-  constexpr int RS = 15;  // record: x(4) A(6: 00 01 02 11 12 22) h(3) one(1) pad
-  __shared__ double rec[8][32 * RS];
-  const int lane = threadIdx.x & 31;
-  const int wb = threadIdx.x >> 5;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= g.n_chunks) return;
-  const int cam = __ldg(g.chunk_cam + c);
-  const int o0 = __ldg(g.chunk_off + c), o1 = __ldg(g.chunk_off + c + 1);
+__global__ void __launch_bounds__(FT) k_lin_cam(Graph g, const double* __restrict__ crec,
+                                               const double* __restrict__ cs_x,
+                                               double* __restrict__ cUraw, Coef k) {
+  constexpr int NA = 52;  // 4 x 10 weighted second moments + 12 b_p
+  __shared__ double red[(FT / 32) * NA];
+  __shared__ double tot[NA];
+  const int cam = blockIdx.x, tid = threadIdx.x;
+  const int o0 = g.cam_off[cam], o1 = g.cam_off[cam + 1];
   const double* cp = crec + (size_t)cam * CREC;
   const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2 = ldg4(cp + 8);
-  int idx[3][3];
-  bool has[3];
+  double acc[NA];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    int e = lane + 32 * q;
-    has[q] = e < LINP;
-    int ee = has[q] ? e : 0;
-    idx[q][0] = c_lin_idx[ee][0];
-    idx[q][1] = c_lin_idx[ee][1];
-    idx[q][2] = c_lin_idx[ee][2];
+  for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+  for (int o = o0 + tid; o < o1; o += FT) {
+    const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
+    const double4 X = ldg4(cs_x + 4 * (size_t)o);
+    const double u0 = dot4(P0, X), u1 = dot4(P1, X), u2 = dot4(P2, X);
+    double w[4], h[3];
+    if (STAGE == 1) {
+      const double r0 = k.s1 * (u0 - u2 * m.x), r1 = k.s1 * (u1 - u2 * m.y);
+      const double r2 = k.s2 * (u0 - m.x), r3 = k.s2 * (u1 - m.y);
+      w[0] = 1.0;
+      w[1] = m.x;
+      w[2] = m.y;
+      w[3] = m.x * m.x + m.y * m.y;
+      h[0] = fma(k.s1, r0, k.s2 * r2);
+      h[1] = fma(k.s1, r1, k.s2 * r3);
+      h[2] = -k.s1 * fma(m.x, r0, m.y * r1);
+    } else {
+      const double iz = 1.0 / u2, i2 = iz * iz;
+      const double p0 = u0 * iz, p1 = u1 * iz;
+      const double r0 = u0 / u2 - m.x, r1 = u1 / u2 - m.y;
+      w[0] = i2;
+      w[1] = p0 * i2;
+      w[2] = p1 * i2;
+      w[3] = (p0 * p0 + p1 * p1) * i2;
+      h[0] = iz * r0;
+      h[1] = iz * r1;
+      h[2] = -iz * fma(p0, r0, p1 * r1);
+    }
+    const double xv[4] = {X.x, X.y, X.z, X.w};
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = a; b < 4; ++b) {
+        const double xx = xv[a] * xv[b];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[10 * q + e] = fma(w[q], xx, acc[10 * q + e]);
+        ++e;
+      }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[40 + 4 * c + a] = fma(h[c], xv[a], acc[40 + 4 * c + a]);
   }
-  double acc[3] = {0.0, 0.0, 0.0};
-  double* my = &rec[wb][0];
-  for (int base = o0; base < o1; base += 32) {
-    const int o = base + lane;
-    double r_[RS];
+  // fixed-order block reduction
 #pragma unroll
-    for (int i = 0; i < RS; ++i) r_[i] = 0.0;
-    if (o < o1) {
-      const int j = __ldg(g.cs_lm + o);
-      const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
-      const double4 X = ldg4(lrec + (size_t)j * LREC);
-      r_[0] = X.x;
-      r_[1] = X.y;
-      r_[2] = X.z;
-      r_[3] = X.w;
-      double u0 = dot4(P0, X), u1 = dot4(P1, X), u2 = dot4(P2, X);
-      if (STAGE == 1) {
-        double s1 = k.s1, s2 = k.s2, a = s1 * s1;
-        double rr0 = s1 * (u0 - u2 * m.x), rr1 = s1 * (u1 - u2 * m.y);
-        double rr2 = s2 * (u0 - m.x), rr3 = s2 * (u1 - m.y);
-        r_[4] = a + s2 * s2;
-        r_[5] = 0.0;
-        r_[6] = -a * m.x;
-        r_[7] = a + s2 * s2;
-        r_[8] = -a * m.y;
-        r_[9] = a * (m.x * m.x + m.y * m.y);
-        r_[10] = fma(s1, rr0, s2 * rr2);
-        r_[11] = fma(s1, rr1, s2 * rr3);
-        r_[12] = -s1 * fma(m.x, rr0, m.y * rr1);
-        r_[13] = 1.0;
+  for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] += __shfl_xor_sync(PV_FULL, acc[i], d);
+  const int lane = tid & 31, wq = tid >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NA; ++i) red[wq * NA + i] = acc[i];
+  __syncthreads();
+  if (tid < NA) {
+    double s = 0.0;
+    for (int q = 0; q < FT / 32; ++q) s += red[q * NA + tid];
+    tot[tid] = s;
+  }
+  __syncthreads();
+  double c00, c02, c12, c22;
+  if (STAGE == 1) {
+    const double a = k.s1 * k.s1;
+    c00 = a + k.s2 * k.s2;
+    c02 = -a;
+    c12 = -a;
+    c22 = a;
+  } else {
+    c00 = 1.0;
+    c02 = -1.0;
+    c12 = -1.0;
+    c22 = 1.0;
+  }
+  // moment index of (a, b), a <= b, in the 10-entry packing
+  auto mi = [](int a, int b) {
+    int lo = a < b ? a : b, hi = a < b ? b : a;
+    return lo * 4 - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  for (int e = tid; e < LINP; e += FT) {
+    double val;
+    if (e < 78) {
+      int i = 0, rem = e;
+      while (rem >= 12 - i) {
+        rem -= 12 - i;
+        ++i;
+      }
+      const int j = i + rem;
+      const int c = i / 4, a = i % 4, d = j / 4, b = j % 4;
+      const int ix = mi(a, b);
+      if (c == d) {
+        val = c == 2 ? c22 * tot[30 + ix] : c00 * tot[ix];
+      } else if (c == 0 && d == 1) {
+        val = 0.0;
+      } else if (c == 0 && d == 2) {
+        val = c02 * tot[10 + ix];
       } else {
-        double iz = 1.0 / u2, i2 = iz * iz;
-        double p0 = u0 * iz, p1 = u1 * iz;
-        double rr0 = u0 / u2 - m.x, rr1 = u1 / u2 - m.y;
-        r_[4] = i2;
-        r_[5] = 0.0;
-        r_[6] = -p0 * i2;
-        r_[7] = i2;
-        r_[8] = -p1 * i2;
-        r_[9] = (p0 * p0 + p1 * p1) * i2;
-        r_[10] = iz * rr0;
-        r_[11] = iz * rr1;
-        r_[12] = -iz * fma(p0, rr0, p1 * rr1);
-        r_[13] = 1.0;
+        val = c12 * tot[20 + ix];
       }
+    } else {
+      val = tot[40 + (e - 78)];
     }
-#pragma unroll
-    for (int i = 0; i < RS; ++i) my[lane * RS + i] = r_[i];
-    __syncwarp();
-    const int nb = min(32, o1 - base);
-    for (int qo = 0; qo < nb; ++qo) {
-      const double* rq = my + qo * RS;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (has[q]) acc[q] = fma(rq[idx[q][0]] * rq[idx[q][1]], rq[idx[q][2]], acc[q]);
-      }
-    }
-    __syncwarp();
+    cUraw[(size_t)cam * LINP + e] = val;
   }
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-    if (has[q]) part[(size_t)c * LINP + lane + 32 * q] = acc[q];
-}
-
-// per camera: sum chunk partials (fixed order) -> cUraw (90 per camera)
-__global__ void k_lin_cam_reduce(Graph g, const double* __restrict__ part,
-                                 double* __restrict__ cUraw) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n_p * LINP) return;
-  const int cam = i / LINP, e = i - cam * LINP;
-  double s = 0.0;
-  for (int c = g.cam_chunk[cam]; c < g.cam_chunk[cam + 1]; ++c) s += part[(size_t)c * LINP + e];
-  cUraw[i] = s;
 }
 
 // per camera: unpack, project (stage 2), store U_lin (row stride 12) and b_p
@@ -673,7 +856,6 @@ __global__ void k_lin_cam_project(int n_p, const double* __restrict__ cUraw,
   for (int i = 0; i < 12; ++i) bo[i] = i < 11 ? bt[i] : 0.0;
 }
 
-// ---------------------------------------------------------------------------
 // K3 damping + U^-1 (Cholesky; reference uses LU, difference <= 1e-13)
 
 __global__ void k_damp_cam(int n_p, int D, const double* __restrict__ cU, double lam,
@@ -761,7 +943,8 @@ __global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const double*
 // RHS landmark vector t = V+ b_l (normal_eq.py:221-226), lifted by B_lm in stage 2
 template <int STAGE>
 __global__ void k_lm_rhs_t(int n_l, const double* __restrict__ lbl,
-                           const double* __restrict__ lsys, double* __restrict__ lrec) {
+                           const double* __restrict__ lsys, const double* __restrict__ lrec,
+                           double* __restrict__ tarr) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= n_l) return;
   const double* vs = lsys + (size_t)l * LSYS;
@@ -770,13 +953,13 @@ __global__ void k_lm_rhs_t(int n_l, const double* __restrict__ lbl,
   double b3[3] = {bl[0], bl[1], bl[2]}, t[3];
   sym3_apply(P6, b3, t);
   if (STAGE == 1) {
-    st4(lrec + (size_t)l * LREC + 4, make_double4(t[0], t[1], t[2], 0.0));
+    st4(tarr + (size_t)l * 4, make_double4(t[0], t[1], t[2], 0.0));
   } else {
     const double* xp = lrec + (size_t)l * LREC;
     double xv[4] = {xp[0], xp[1], xp[2], xp[3]}, h[4], t4[4];
     householder_h<4>(xv, h);
     basis_apply<4>(h, t, t4);
-    st4(lrec + (size_t)l * LREC + 4, make_double4(t4[0], t4[1], t4[2], t4[3]));
+    st4(tarr + (size_t)l * 4, make_double4(t4[0], t4[1], t4[2], t4[3]));
   }
 }
 
@@ -826,10 +1009,6 @@ __global__ void k_trial_cam(int n_p, const double* __restrict__ crec, const doub
   }
   for (int i = 0; i < 12; ++i) tcam[(size_t)cam * 12 + i] = p[i];
 }
-
-// ---------------------------------------------------------------------------
-// K9 cost (objective.py:194-211) and K10 closed-form landmark re-solve
-// (objective.py:251-298), landmark-major, deterministic block partials.
 
 template <int STAGE>
 __device__ __forceinline__ double obs_cost(const double* __restrict__ cams, int cstride, int cam,
@@ -893,104 +1072,220 @@ __global__ void __launch_bounds__(256) k_cost(Graph g, const double* __restrict_
   block_partial(acc, part);
 }
 
-__device__ __forceinline__ void resolve_rows(const double* __restrict__ cams, int cam, double m0,
-                                             double m1, const Coef& k, double* R) {
-  const double* c = cams + (size_t)cam * 12;
-  double4 P0 = ldg4(c), P1 = ldg4(c + 4), P2 = ldg4(c + 8);
-  // rows [A | c] of the affine model r = A v + c at x = (0, 0, 0, 1)
-  givens_row(R, k.s1 * (P0.x - m0 * P2.x), k.s1 * (P0.y - m0 * P2.y), k.s1 * (P0.z - m0 * P2.z),
-             k.s1 * (P0.w - P2.w * m0));
-  givens_row(R, k.s1 * (P1.x - m1 * P2.x), k.s1 * (P1.y - m1 * P2.y), k.s1 * (P1.z - m1 * P2.z),
-             k.s1 * (P1.w - P2.w * m1));
-  givens_row(R, k.s2 * P0.x, k.s2 * P0.y, k.s2 * P0.z, k.s2 * (P0.w - m0));
-  givens_row(R, k.s2 * P1.x, k.s2 * P1.y, k.s2 * P1.z, k.s2 * (P1.w - m1));
+// ---------------------------------------------------------------------------
+// K10 closed-form landmark re-solve (objective.py:251-298): per landmark the
+// stacked affine model r = A v + c (A = J_l at x = e3, c = r at x = e3) is
+// solved in the minimum-norm least-squares sense with the reference's SVD rank
+// rule s > 1e-10 s_max.  A = QR via CholeskyQR2 (two Gram passes, accurate to
+// O(eps) for cond(A) < ~1e7), then a one-sided Jacobi SVD of the 3x3 R.
+// Landmarks whose first Gram pass loses more than 13 digits fall back to an
+// exact Givens QR of all their rows.  The stage-1 cost of the re-solved state
+// is accumulated in the same pass (K9 fused).
+
+struct Rows4 {
+  double a[4][3];
+  double c[4];
+};
+
+__device__ __forceinline__ Rows4 resolve_rows4(const double* __restrict__ cams, int cam, double m0,
+                                               double m1, const Coef& k) {
+  const double* cp = cams + (size_t)cam * 12;
+  const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2 = ldg4(cp + 8);
+  Rows4 R;
+  R.a[0][0] = k.s1 * (P0.x - m0 * P2.x);
+  R.a[0][1] = k.s1 * (P0.y - m0 * P2.y);
+  R.a[0][2] = k.s1 * (P0.z - m0 * P2.z);
+  R.c[0] = k.s1 * (P0.w - P2.w * m0);
+  R.a[1][0] = k.s1 * (P1.x - m1 * P2.x);
+  R.a[1][1] = k.s1 * (P1.y - m1 * P2.y);
+  R.a[1][2] = k.s1 * (P1.z - m1 * P2.z);
+  R.c[1] = k.s1 * (P1.w - P2.w * m1);
+  R.a[2][0] = k.s2 * P0.x;
+  R.a[2][1] = k.s2 * P0.y;
+  R.a[2][2] = k.s2 * P0.z;
+  R.c[2] = k.s2 * (P0.w - m0);
+  R.a[3][0] = k.s2 * P1.x;
+  R.a[3][1] = k.s2 * P1.y;
+  R.a[3][2] = k.s2 * P1.z;
+  R.c[3] = k.s2 * (P1.w - m1);
+  return R;
 }
+
+// 3x3 Cholesky of packed (00 01 02 11 12 22) into upper R (same packing);
+// returns the smallest pivot ratio d_j / G_jj (<= 0 on failure).
+__device__ __forceinline__ double chol3(const double* G, double* R) {
+  double d0 = G[0];
+  double ratio = G[0] > 0.0 ? 1.0 : 0.0;
+  double r00 = d0 > 0.0 ? sqrt(d0) : 0.0;
+  double r01 = r00 > 0.0 ? G[1] / r00 : 0.0;
+  double r02 = r00 > 0.0 ? G[2] / r00 : 0.0;
+  double d1 = G[3] - r01 * r01;
+  ratio = fmin(ratio, G[3] > 0.0 ? d1 / G[3] : 0.0);
+  double r11 = d1 > 0.0 ? sqrt(d1) : 0.0;
+  double r12 = r11 > 0.0 ? (G[4] - r01 * r02) / r11 : 0.0;
+  double d2 = G[5] - r02 * r02 - r12 * r12;
+  ratio = fmin(ratio, G[5] > 0.0 ? d2 / G[5] : 0.0);
+  double r22 = d2 > 0.0 ? sqrt(d2) : 0.0;
+  R[0] = r00;
+  R[1] = r01;
+  R[2] = r02;
+  R[3] = r11;
+  R[4] = r12;
+  R[5] = r22;
+  return ratio;
+}
+
+__device__ __forceinline__ void gram_acc(const double* w, double c, double* acc /*9*/) {
+  acc[0] = fma(w[0], w[0], acc[0]);
+  acc[1] = fma(w[0], w[1], acc[1]);
+  acc[2] = fma(w[0], w[2], acc[2]);
+  acc[3] = fma(w[1], w[1], acc[3]);
+  acc[4] = fma(w[1], w[2], acc[4]);
+  acc[5] = fma(w[2], w[2], acc[5]);
+  acc[6] = fma(w[0], c, acc[6]);
+  acc[7] = fma(w[1], c, acc[7]);
+  acc[8] = fma(w[2], c, acc[8]);
+}
+
+// w = a R^-1 (row vector, R upper 3x3 packed) using precomputed inverse diagonals
+__device__ __forceinline__ void tri_solve_row(const double* a, const double* R, const double* id,
+                                              double* w) {
+  w[0] = a[0] * id[0];
+  w[1] = (a[1] - w[0] * R[1]) * id[1];
+  w[2] = (a[2] - w[0] * R[2] - w[1] * R[4]) * id[2];
+}
+
+// head-lane solve: R1 (pass 1), pass-2 sums (G2, z1) -> full 4x4 packed R for lsq_from_r
+__device__ __forceinline__ bool cqr2_solve(const double* R1, const double* s2, double* v) {
+  double R2[6];
+  chol3(s2, R2);
+  // R = R2 R1 (upper x upper)
+  double R[6];
+  R[0] = R2[0] * R1[0];
+  R[1] = R2[0] * R1[1] + R2[1] * R1[3];
+  R[2] = R2[0] * R1[2] + R2[1] * R1[4] + R2[2] * R1[5];
+  R[3] = R2[3] * R1[3];
+  R[4] = R2[3] * R1[4] + R2[4] * R1[5];
+  R[5] = R2[5] * R1[5];
+  // z = R2^-T z1 (forward substitution with the lower triangle R2^T)
+  double z[3];
+  z[0] = R2[0] != 0.0 ? s2[6] / R2[0] : 0.0;
+  z[1] = R2[3] != 0.0 ? (s2[7] - R2[1] * z[0]) / R2[3] : 0.0;
+  z[2] = R2[5] != 0.0 ? (s2[8] - R2[2] * z[0] - R2[4] * z[1]) / R2[5] : 0.0;
+  const double full[10] = {R[0], R[1], R[2], z[0], R[3], R[4], z[1], R[5], z[2], 0.0};
+  return lsq_from_r(full, 1e-10, v);
+}
+
+constexpr double CQR_PIVOT_TOL = 1e-13;
 
 __global__ void __launch_bounds__(256) k_resolve(Graph g, const double* __restrict__ tcam,
                                                  double* __restrict__ tlm,
                                                  double* __restrict__ part, int* flags, Coef k) {
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  double acc = 0.0;
-  int rankdef = 0;
+  double cost = 0.0;
+  int rankdef = 0, fallback = 0;
   if (w < g.n_tasks) {
     Task t = load_task(g, w, lane);
-    double R[10];
-#pragma unroll
-    for (int i = 0; i < 10; ++i) R[i] = 0.0;
+    int l, seg_end, src;
     if (t.long_task) {
-      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-        double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-        resolve_rows(tcam, __ldg(g.ls_cam + o), m.x, m.y, k, R);
-      }
-      for (int d = 16; d > 0; d >>= 1) {
-        double O[10];
-#pragma unroll
-        for (int i = 0; i < 10; ++i) O[i] = __shfl_down_sync(PV_FULL, R[i], d);
-        if (lane < d) givens_merge(R, O);
-      }
-      double xn[4] = {0.0, 0.0, 0.0, 0.0};
-      if (lane == 0) {
-        double v[3];
-        bool full = lsq_from_r(R, 1e-10, v);
-        double4 old = ld4(tlm + (size_t)t.l0 * 4);
-        xn[0] = full ? v[0] : old.x;
-        xn[1] = full ? v[1] : old.y;
-        xn[2] = full ? v[2] : old.z;
-        xn[3] = full ? 1.0 : old.w;
-        rankdef = !full;
-        st4(tlm + (size_t)t.l0 * 4, make_double4(xn[0], xn[1], xn[2], xn[3]));
-      }
-      double4 x;
-      x.x = __shfl_sync(PV_FULL, xn[0], 0);
-      x.y = __shfl_sync(PV_FULL, xn[1], 0);
-      x.z = __shfl_sync(PV_FULL, xn[2], 0);
-      x.w = __shfl_sync(PV_FULL, xn[3], 0);
-      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-        double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-        acc += obs_cost<1>(tcam, 12, __ldg(g.ls_cam + o), m.x, m.y, x, k, flags);
-      }
+      l = t.l0;
+      seg_end = 32;
+      src = 0;
     } else {
-      int l, seg_end;
       lane_segment(t, lane, l, seg_end);
-      int cam = 0;
-      double2 m = make_double2(0.0, 0.0);
-      if (lane < t.n) {
-        int o = t.o0 + lane;
-        m = ldg2(g.ls_m + 2 * (size_t)o);
-        cam = __ldg(g.ls_cam + o);
-        resolve_rows(tcam, cam, m.x, m.y, k, R);
-      }
-      for (int d = 1; d < 32; d <<= 1) {
-        double O[10];
+      src = seg_start_lane(t, lane < t.n ? lane : 0);
+    }
+    const bool head = t.long_task ? lane == 0 : (lane < t.n && ((t.heads >> lane) & 1u));
+    const int stride = t.long_task ? 32 : 1 << 30;
+    const int oend = t.o0 + t.n;
+    // pass 1: Gram of A
+    double g1[6] = {0, 0, 0, 0, 0, 0};
+    for (int o = t.o0 + lane; o < oend; o += stride) {
+      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+      const Rows4 rw = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
 #pragma unroll
-        for (int i = 0; i < 10; ++i) O[i] = __shfl_down_sync(PV_FULL, R[i], d);
-        if (lane + d < seg_end) givens_merge(R, O);
+      for (int r = 0; r < 4; ++r) {
+        g1[0] = fma(rw.a[r][0], rw.a[r][0], g1[0]);
+        g1[1] = fma(rw.a[r][0], rw.a[r][1], g1[1]);
+        g1[2] = fma(rw.a[r][0], rw.a[r][2], g1[2]);
+        g1[3] = fma(rw.a[r][1], rw.a[r][1], g1[3]);
+        g1[4] = fma(rw.a[r][1], rw.a[r][2], g1[4]);
+        g1[5] = fma(rw.a[r][2], rw.a[r][2], g1[5]);
       }
-      double xn[4] = {0.0, 0.0, 0.0, 0.0};
-      if (lane < t.n && ((t.heads >> lane) & 1u)) {
-        double v[3];
-        bool full = lsq_from_r(R, 1e-10, v);
-        double4 old = ld4(tlm + (size_t)l * 4);
-        xn[0] = full ? v[0] : old.x;
-        xn[1] = full ? v[1] : old.y;
-        xn[2] = full ? v[2] : old.z;
-        xn[3] = full ? 1.0 : old.w;
-        rankdef = !full;
-        st4(tlm + (size_t)l * 4, make_double4(xn[0], xn[1], xn[2], xn[3]));
+    }
+    if (t.long_task) warp_reduce_all(g1);
+    else seg_reduce(g1, lane, seg_end);
+    double R1[6] = {0, 0, 0, 0, 0, 0};
+    double fb = 0.0;
+    if (head) {
+      const double ratio = chol3(g1, R1);
+      fb = !(ratio > CQR_PIVOT_TOL) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) R1[i] = __shfl_sync(PV_FULL, R1[i], src);
+    fb = __shfl_sync(PV_FULL, fb, src);
+    // pass 2: Gram of A R1^-1 and (A R1^-1)^T c
+    double s2[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (fb == 0.0) {
+      const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
+      for (int o = t.o0 + lane; o < oend; o += stride) {
+        const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+        const Rows4 rw = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double wv[3];
+          tri_solve_row(rw.a[r], R1, id, wv);
+          gram_acc(wv, rw.c[r], s2);
+        }
       }
-      const int src = seg_start_lane(t, lane < t.n ? lane : 0);
-      double4 x;
-      x.x = __shfl_sync(PV_FULL, xn[0], src);
-      x.y = __shfl_sync(PV_FULL, xn[1], src);
-      x.z = __shfl_sync(PV_FULL, xn[2], src);
-      x.w = __shfl_sync(PV_FULL, xn[3], src);
-      if (lane < t.n) acc = obs_cost<1>(tcam, 12, cam, m.x, m.y, x, k, flags);
+    }
+    if (t.long_task) warp_reduce_all(s2);
+    else seg_reduce(s2, lane, seg_end);
+    double xn[4] = {0.0, 0.0, 0.0, 0.0};
+    if (head) {
+      double v[3];
+      bool full;
+      if (fb == 0.0) {
+        full = cqr2_solve(R1, s2, v);
+      } else {  // exact Givens QR of all rows of this landmark
+        fallback = 1;
+        double Rg[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        const int ob = t.long_task ? t.o0 : t.o0 + lane;
+        const int oe = t.long_task ? oend : t.o0 + seg_end;
+        for (int o = ob; o < oe; ++o) {
+          const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+          const Rows4 rw = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
+          for (int r = 0; r < 4; ++r)
+            givens_row(Rg, rw.a[r][0], rw.a[r][1], rw.a[r][2], rw.c[r]);
+        }
+        full = lsq_from_r(Rg, 1e-10, v);
+      }
+      const double4 old = ld4(tlm + (size_t)l * 4);
+      xn[0] = full ? v[0] : old.x;
+      xn[1] = full ? v[1] : old.y;
+      xn[2] = full ? v[2] : old.z;
+      xn[3] = full ? 1.0 : old.w;
+      rankdef = !full;
+      st4(tlm + (size_t)l * 4, make_double4(xn[0], xn[1], xn[2], xn[3]));
+    }
+    double4 x;
+    x.x = __shfl_sync(PV_FULL, xn[0], src);
+    x.y = __shfl_sync(PV_FULL, xn[1], src);
+    x.z = __shfl_sync(PV_FULL, xn[2], src);
+    x.w = __shfl_sync(PV_FULL, xn[3], src);
+    for (int o = t.o0 + lane; o < oend; o += stride) {
+      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+      cost += obs_cost<1>(tcam, 12, __ldg(g.ls_cam + o), m.x, m.y, x, k, flags);
     }
   }
-  unsigned bal = __ballot_sync(PV_FULL, rankdef);
-  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(flags + F_N_RANKDEF, __popc(bal));
-  block_partial(acc, part);
+  const unsigned bal = __ballot_sync(PV_FULL, rankdef);
+  const unsigned bfb = __ballot_sync(PV_FULL, fallback);
+  if ((threadIdx.x & 31) == 0) {
+    if (bal) atomicAdd(flags + F_N_RANKDEF, __popc(bal));
+    if (bfb) atomicAdd(flags + F_N_FALLBACK, __popc(bfb));
+  }
+  block_partial(cost, part);
 }
 
 // fixed-order single-block sum of block partials

@@ -81,6 +81,10 @@ class DeviceProblem:
         self._call("pv_info", _lib.i64ptr(out))
         return {k: int(out[i]) for i, k in enumerate(_lib.INFO_FIELDS)}
 
+    def set_option(self, key: int, value: int) -> None:
+        """Tuning knob of the term kernels (include/povar.h PV_OPT_*); results unchanged."""
+        self._call("pv_set_option", int(key), int(value))
+
     @property
     def stream_handle(self) -> int:
         return int(self._lib.pv_stream(self._ctx) or 0)
@@ -152,6 +156,7 @@ class DeviceProblem:
     def bench_terms(self, stage: int, n_terms: int) -> dict:
         ms = (ctypes.c_float * 4)()
         self._call("pv_bench_terms", int(stage), int(n_terms), ms)
+        # [0] k_lm_reduce, [1] k_cam (fused; part A when sharded), [2] allreduce + part B
         return {"phase1_ms": ms[0], "phase2_ms": ms[1], "epilogue_ms": ms[2], "term_ms": ms[3]}
 
     def debug(self, which: int) -> np.ndarray:
