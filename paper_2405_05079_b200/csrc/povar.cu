@@ -628,21 +628,29 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
   API_END(c)
 }
 
+// true when this shard's observed landmarks are exactly the contiguous global
+// rows lm_gid[0] .. lm_gid[0] + n_ls - 1 (direct host <-> device copies)
+static bool lm_contiguous(const pv_ctx* c) {
+  return c->n_ls == 0 || c->lm_gid.back() - c->lm_gid.front() + 1 == (int64_t)c->n_ls;
+}
+
 int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
-  std::vector<double> lm_local((size_t)c->n_ls * 4);
-  for (int j = 0; j < c->n_ls; ++j)
-    for (int q = 0; q < 4; ++q) lm_local[(size_t)j * 4 + q] = lms[c->lm_gid[j] * 4 + q];
-  double* dc = c->ctmp;  // n_p*12
-  CK(cudaMemcpyAsync(dc, cams, sizeof(double) * c->n_p * 12, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->tlm, lm_local.data(), sizeof(double) * lm_local.size(),
-                     cudaMemcpyHostToDevice, c->stream));
-  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
-  k_put_state<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, dc, c->tlm,
-                                                         c->crec, c->lrec);
-  c->launched();
-  c->check_launch();
+  CK(cudaMemcpy2DAsync(c->crec, CREC * sizeof(double), cams, 12 * sizeof(double),
+                       12 * sizeof(double), c->n_p, cudaMemcpyHostToDevice, c->stream));
+  std::vector<double> lm_local;
+  if (c->n_ls > 0) {
+    const double* src = lms + c->lm_gid.front() * 4;
+    if (!lm_contiguous(c)) {
+      lm_local.resize((size_t)c->n_ls * 4);
+      for (int j = 0; j < c->n_ls; ++j)
+        for (int q = 0; q < 4; ++q) lm_local[(size_t)j * 4 + q] = lms[c->lm_gid[j] * 4 + q];
+      src = lm_local.data();
+    }
+    CK(cudaMemcpyAsync(c->lrec, src, sizeof(double) * 4 * c->n_ls, cudaMemcpyHostToDevice,
+                       c->stream));
+  }
   c->sync();
   c->lin_stage = 0;
   c->vp_cached = false;
@@ -650,47 +658,37 @@ int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
 }
 
 static void get_state_impl(pv_ctx* c, const double* dcam, int cstride, const double* dlm,
-                           int lstride, double* cams, double* lms) {
-  double* tc = c->ctmp;
-  std::vector<double> lm_local((size_t)c->n_ls * 4);
-  double* tl = nullptr;
-  // gather into contiguous scratch (reuse cpart-sized buffers through a temp alloc)
-  tl = c->alloc<double>((size_t)c->n_ls * 4);
-  const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
-  if (cstride == CREC) {
-    k_get_state<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, dcam, dlm, tc,
-                                                           tl);
-    c->launched();
-  } else {
-    CK(cudaMemcpyAsync(tc, dcam, sizeof(double) * c->n_p * 12, cudaMemcpyDeviceToDevice,
-                       c->stream));
-    CK(cudaMemcpyAsync(tl, dlm, sizeof(double) * c->n_ls * 4, cudaMemcpyDeviceToDevice,
-                       c->stream));
+                           double* cams, double* lms) {
+  CK(cudaMemcpy2DAsync(cams, 12 * sizeof(double), dcam, cstride * sizeof(double),
+                       12 * sizeof(double), c->n_p, cudaMemcpyDeviceToHost, c->stream));
+  if (c->n_ls > 0) {
+    if (lm_contiguous(c)) {
+      CK(cudaMemcpyAsync(lms + c->lm_gid.front() * 4, dlm, sizeof(double) * 4 * c->n_ls,
+                         cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    } else {
+      std::vector<double> lm_local((size_t)c->n_ls * 4);
+      CK(cudaMemcpyAsync(lm_local.data(), dlm, sizeof(double) * lm_local.size(),
+                         cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      for (int j = 0; j < c->n_ls; ++j)
+        for (int q = 0; q < 4; ++q) lms[c->lm_gid[j] * 4 + q] = lm_local[(size_t)j * 4 + q];
+    }
   }
-  (void)lstride;
-  CK(cudaMemcpyAsync(cams, tc, sizeof(double) * c->n_p * 12, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(lm_local.data(), tl, sizeof(double) * lm_local.size(),
-                     cudaMemcpyDeviceToHost, c->stream));
   c->sync();
-  // release the temporary
-  cudaFree(tl);
-  c->allocs.pop_back();
-  c->device_bytes -= std::max<size_t>((size_t)c->n_ls * 4, 1) * sizeof(double);
-  for (int j = 0; j < c->n_ls; ++j)
-    for (int q = 0; q < 4; ++q) lms[c->lm_gid[j] * 4 + q] = lm_local[(size_t)j * 4 + q];
 }
 
 int pv_get_state(pv_ctx* c, double* cams, double* lms) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
-  get_state_impl(c, c->crec, CREC, c->lrec, LREC, cams, lms);
+  get_state_impl(c, c->crec, CREC, c->lrec, cams, lms);
   API_END(c)
 }
 
 int pv_get_trial(pv_ctx* c, double* cams, double* lms) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
-  get_state_impl(c, c->tcam, 12, c->tlm, 4, cams, lms);
+  get_state_impl(c, c->tcam, 12, c->tlm, cams, lms);
   API_END(c)
 }
 

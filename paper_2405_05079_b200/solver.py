@@ -98,9 +98,15 @@ class DeviceProblem:
         self._call("pv_set_state", _lib.dptr(cams), _lib.dptr(lms))
         self._state_template = lms
 
-    def get_state(self, trial: bool = False) -> ProjectiveState:
+    def get_state(self, trial: bool = False, out: ProjectiveState | None = None
+                  ) -> ProjectiveState:
+        """Download the (trial) state.  Landmarks this shard does not own (unobserved or
+        other ranks') keep the values of the last uploaded state."""
         cams = np.empty((self.n_p, 3, 4))
-        lms = np.array(self._state_template, copy=True)
+        if self.n_l_local == self.problem.num_landmarks:
+            lms = np.empty((self.problem.num_landmarks, 4))
+        else:
+            lms = np.array(self._state_template, copy=True)
         self._call("pv_get_trial" if trial else "pv_get_state", _lib.dptr(cams), _lib.dptr(lms))
         return ProjectiveState(cams, lms)
 

@@ -1,0 +1,130 @@
+"""CPU: host-side logic, API types, the C-ABI library surface and the generator."""
+
+import ast
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_solver_config_validation_mirrors_reference():
+    from paper_2405_05079_b200 import SolverConfig, PoseConfig
+    cfg = SolverConfig()
+    assert (cfg.max_outer_iterations, cfg.function_tolerance, cfg.initial_lambda,
+            cfg.max_power_order, cfg.power_threshold, cfg.max_inner_iterations,
+            cfg.pose.eta) == (50, 1e-6, 1e-4, 20, 0.01, 500, 0.1)
+    for bad in (dict(inner_solver="magic"), dict(mode="alternation"),
+                dict(initial_lambda=0.0), dict(max_power_order=-1)):
+        with pytest.raises(ValueError):
+            SolverConfig(**bad)
+    with pytest.raises(ValueError):
+        PoseConfig(1.5)
+
+
+def test_problem_and_state_validation():
+    from paper_2405_05079_b200 import BaProblem, ProjectiveState
+    with pytest.raises(ValueError):
+        BaProblem(2, 1, 1, np.array([2]), np.array([0]), np.zeros((1, 2)))
+    with pytest.raises(ValueError):
+        BaProblem(2, 1, 2, np.array([0]), np.array([0]), np.zeros((1, 2)))
+    with pytest.raises(ValueError):
+        ProjectiveState(np.zeros((2, 4, 3)), np.zeros((1, 4)))
+    p = BaProblem(2, 1, 1, np.array([1]), np.array([0]), np.zeros((1, 2)))
+    assert not p.measurements.flags.writeable
+
+
+def test_trace_and_labels():
+    from paper_2405_05079_b200 import ConvergenceTrace, SolverConfig, TraceRecord, solver_label
+    with pytest.raises(ValueError):
+        ConvergenceTrace("a", "p", "stage1", [TraceRecord(0, 1.0, 0.0), TraceRecord(1, 0.5, -1)],
+                         1.0)
+    assert solver_label(1, SolverConfig()) == "povar"
+    assert solver_label(1, SolverConfig(mode="joint")) == "poba"
+    assert solver_label(2, SolverConfig()) == "ripoba"
+
+
+def test_header_symbols_are_bound_and_exported():
+    """Every entry point declared in include/povar.h is exported by libpovar.so and bound."""
+    from paper_2405_05079_b200 import _lib
+    header = (ROOT / "include" / "povar.h").read_text()
+    declared = set(re.findall(r"\b(pv_[a-z_0-9]+)\s*\(", header))
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    assert declared == bound, declared ^ bound
+    lib = _lib.load()  # loading needs no GPU
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    import paper_2405_05079_b200 as pv
+    from paper_2405_05079_b200 import synth
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present; the loud-failure path is exercised on CPU hosts")
+    pr, _ = synth.make_problem("tiny", 0)
+    with pytest.raises(RuntimeError):
+        pv.DeviceProblem(pr, 0.1)
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = ROOT / "paper_2405_05079_b200"
+    for path in pkg.rglob("*.py"):
+        tree = ast.parse(path.read_text())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                names = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom):
+                names = [node.module or ""]
+            else:
+                continue
+            assert not any(n.split(".")[0] == "oracle" for n in names), path
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_plan_tiles_and_balances(world):
+    from paper_2405_05079_b200 import shard, synth
+    pr, _ = synth.make_problem("small", 0)
+    plan = shard.plan_shards(pr, world)
+    assert plan[0][0] == 0 and plan[-1][1] == pr.num_landmarks
+    assert all(a[1] == b[0] for a, b in zip(plan, plan[1:]))
+    counts = shard.shard_observation_counts(pr, plan)
+    assert sum(counts) == pr.num_observations
+    ideal = pr.num_observations / world
+    assert max(counts) - ideal <= 64  # one landmark's worth of slack
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_generator_matches_config(name):
+    from paper_2405_05079_b200 import synth
+    cfg = synth.CONFIGS[name]
+    pr, truth = synth.make_problem(name, 0)
+    assert (pr.num_cameras, pr.num_landmarks) == (cfg.n_cameras, cfg.n_landmarks)
+    k = np.bincount(pr.landmark_indices, minlength=pr.num_landmarks)
+    assert k.min() >= 2
+    if name == "tiny":
+        assert k.max() <= 6
+    pairs = pr.camera_indices * pr.num_landmarks + pr.landmark_indices
+    assert len(np.unique(pairs)) == pr.num_observations  # distinct cameras per landmark
+    # noise-free ground truth reproduces the measurements to ~1 px / mean focal
+    gt = synth.ground_truth_state(truth)
+    u = np.einsum("nij,nj->ni", gt.cameras[pr.camera_indices], gt.landmarks[pr.landmark_indices])
+    assert np.all(u[:, 2] > 0)
+    err = np.abs(u[:, :2] / u[:, 2:] - pr.measurements).max() * truth["focal_mean"]
+    assert err < 6.0
+    # deterministic
+    pr2, _ = synth.make_problem(name, 0)
+    np.testing.assert_array_equal(pr.measurements, pr2.measurements)
+
+
+def test_retract_and_lift():
+    import paper_2405_05079_b200 as pv
+    st = pv.ProjectiveState(np.arange(24.0).reshape(2, 3, 4) + 1, np.ones((3, 4)))
+    r = pv.lift_stage1_to_stage2(st)
+    np.testing.assert_allclose(np.linalg.norm(r.cameras.reshape(-1, 12), axis=1), 1.0)
+    np.testing.assert_allclose(np.linalg.norm(r.landmarks, axis=1), 1.0)
+    with pytest.raises(ValueError):
+        pv.retract(pv.ProjectiveState(np.zeros((1, 3, 4)), np.ones((1, 4))))
