@@ -62,7 +62,8 @@ enum {
 enum {
   PV_INFO_NP = 0, PV_INFO_NL_LOCAL = 1, PV_INFO_NO_LOCAL = 2, PV_INFO_TASKS = 3,
   PV_INFO_CHUNKS = 4, PV_INFO_LAUNCHES = 5, PV_INFO_RANK = 6, PV_INFO_WORLD = 7,
-  PV_INFO_DEVICE_BYTES = 8, PV_INFO_NL_GLOBAL = 9, PV_INFO_COUNT = 16
+  PV_INFO_DEVICE_BYTES = 8, PV_INFO_NL_GLOBAL = 9, PV_INFO_RESOLVE_FALLBACKS = 10,
+  PV_INFO_BLOCKS = 11, PV_INFO_COUNT = 16
 };
 
 /* tuning knobs of the term kernels (pv_set_option); results do not depend on them */
@@ -70,7 +71,9 @@ enum {
   PV_OPT_STAGE_CAP = 0,   /* observations per camera staged in shared memory (0..2048)     */
   PV_OPT_POL_STREAM = 1,  /* L2 priority of camera-sorted streams: 0 normal 1 first 2 last */
   PV_OPT_POL_T = 2,       /* L2 priority of the gathered landmark vectors t              */
-  PV_OPT_POL_S = 3        /* L2 priority of the per-observation partials s               */
+  PV_OPT_POL_S = 3,       /* L2 priority of the per-observation partials s               */
+  PV_OPT_DISCARD_S = 4,   /* 1: drop consumed partials from L2 without write-back          */
+  PV_OPT_BLOCK_BYTES = 5  /* L2 budget of one landmark block's partials (re-blocks)        */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the
@@ -139,8 +142,9 @@ int pv_get_step(pv_ctx* ctx, double* dx, double* dl);
 int pv_schur_apply(pv_ctx* ctx, int stage, const double* v, double* out);
 
 /* Timed power-series terms (no stop test), for the bench: runs n_terms terms on
- * the context stream and returns the mean device ms of phase1, phase2,
- * epilogue and a whole term in ms[0..3]. */
+ * the context stream and returns mean device ms per term of k_lm_reduce and of
+ * k_cam (measured on block 0, scaled by the block count), the block count, and
+ * the whole term (event to event) in ms[0..3]. */
 int pv_bench_terms(pv_ctx* ctx, int stage, int n_terms, float* ms);
 
 int pv_debug_get(pv_ctx* ctx, int which, double* out);

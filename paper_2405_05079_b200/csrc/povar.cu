@@ -67,19 +67,25 @@ struct pv_ctx {
   // graph (device)
   Graph g{};
   int *d_ls_cam = nullptr, *d_lm_off = nullptr, *d_task_lm = nullptr, *d_cs_lm = nullptr,
-      *d_cs_pos = nullptr, *d_cam_off = nullptr, *d_ls2cs = nullptr;
+      *d_cs_pos = nullptr, *d_cam_off = nullptr, *d_cam_blk = nullptr;
+  // host copies kept for re-blocking (pv_set_option PV_OPT_BLOCK_BYTES)
+  std::vector<int> h_cs_lm, h_cam_off, h_task_desc;
+  std::vector<int> blk_task;  // [n_blk+1] task boundaries of the landmark blocks
+  int n_blk = 1;
+  int64_t block_bytes = 48ll << 20;
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
   double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam, *tarr, *cs_x, *sbuf;
-  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
+  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
   int* flags;
   unsigned* ticket;
   PowerCtl* ctl;
   PowerCtl* host_ctl = nullptr;  // mapped pinned mirror
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{1792, 0, 0, 0};
+  Tune tune{0, 1, 2, 2, 1};
+  int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
   int step_stage = 0;
@@ -170,7 +176,7 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   std::vector<int> cam_off(n_p + 1, 0);
   for (int64_t k = 0; k < n_os; ++k) cam_off[ls_cam[k] + 1]++;
   for (int64_t i = 0; i < n_p; ++i) cam_off[i + 1] += cam_off[i];
-  std::vector<int> cs_lm(n_os), cs_pos(n_os), ls2cs(n_os);
+  std::vector<int> cs_lm(n_os), cs_pos(n_os);
   std::vector<double> cs_m(2 * n_os);
   {
     std::vector<int> pos(cam_off.begin(), cam_off.end() - 1);
@@ -178,7 +184,6 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
       int p = pos[ls_cam[k]]++;
       cs_lm[p] = ls_lid[k];
       cs_pos[p] = (int)k;
-      ls2cs[k] = p;
       cs_m[2 * p] = ls_m[2 * k];
       cs_m[2 * p + 1] = ls_m[2 * k + 1];
     }
@@ -237,8 +242,10 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->d_cs_m = up_d(cs_m);
   c->d_cs_pos = up_i(cs_pos);
   c->d_cam_off = up_i(cam_off);
-  c->d_ls2cs = up_i(ls2cs);
   c->sync();  // host vectors go out of scope
+  c->h_cs_lm.assign(cs_lm.begin(), cs_lm.begin() + n_os);
+  c->h_cam_off = cam_off;
+  c->h_task_desc = task_desc;
 
   Graph& g = c->g;
   g.n_p = (int)n_p;
@@ -253,7 +260,50 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   g.cs_m = c->d_cs_m;
   g.cs_pos = c->d_cs_pos;
   g.cam_off = c->d_cam_off;
-  g.ls2cs = c->d_ls2cs;
+}
+
+// Landmark blocks of the L2-blocked term: contiguous task ranges with ~equal
+// observation counts, sized so one block's partials s (32 B/obs) fit in the
+// budget; per camera, the camera-sorted sub-range of each block.
+static void build_blocks(pv_ctx* c) {
+  const int n_os = c->n_os, n_tasks = c->n_tasks;
+  const int64_t want = std::max<int64_t>(1, ((int64_t)n_os * 32 + c->block_bytes - 1) /
+                                                std::max<int64_t>(c->block_bytes, 1));
+  const int nb = (int)std::min<int64_t>(want, std::max(1, n_tasks));
+  std::vector<int> bt(1, 0);
+  int64_t cum = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    cum += c->h_task_desc[4 * t + 1];
+    if ((int)bt.size() < nb && cum * nb >= (int64_t)bt.size() * n_os && t + 1 < n_tasks)
+      bt.push_back(t + 1);
+  }
+  bt.push_back(n_tasks);
+  const int B = (int)bt.size() - 1;
+  std::vector<int> lm_first(B + 1);
+  for (int b = 0; b < B; ++b) lm_first[b] = n_tasks ? c->h_task_desc[4 * bt[b] + 2] : 0;
+  lm_first[B] = c->n_ls;
+  std::vector<int> cb((size_t)c->n_p * (B + 1));
+  for (int64_t cam = 0; cam < c->n_p; ++cam) {
+    const int o0 = c->h_cam_off[cam], o1 = c->h_cam_off[cam + 1];
+    int o = o0;
+    for (int b = 0; b <= B; ++b) {
+      while (o < o1 && c->h_cs_lm[o] < lm_first[b]) ++o;
+      cb[(size_t)cam * (B + 1) + b] = (b == B) ? o1 : o;
+    }
+  }
+  if (c->d_cam_blk) {
+    CK(cudaFree(c->d_cam_blk));
+    auto it = std::find(c->allocs.begin(), c->allocs.end(), (void*)c->d_cam_blk);
+    if (it != c->allocs.end()) c->allocs.erase(it);
+  }
+  c->d_cam_blk = c->alloc<int>(cb.size());
+  CK(cudaMemcpyAsync(c->d_cam_blk, cb.data(), cb.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->stream));
+  c->sync();
+  c->blk_task = bt;
+  c->n_blk = B;
+  c->g.n_blk = B;
+  c->g.cam_blk = c->d_cam_blk;
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -262,7 +312,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->lrec = c->alloc<double>(nl * LREC);
   c->lsys = c->alloc<double>(nl * LSYS);
   c->lvr = c->alloc<double>(nl * 8);
-  c->tarr = c->alloc<double>((size_t)c->n_os * 4);  // t per camera-sorted observation
+  c->tarr = c->alloc<double>(nl * 4);  // t per landmark
   c->cs_x = c->alloc<double>((size_t)c->n_os * 4);
   c->sbuf = c->alloc<double>((size_t)c->n_os * 4);
   c->lbl = c->alloc<double>(nl * 4);
@@ -276,6 +326,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->cx = c->alloc<double>(np * 12);
   c->crhs = c->alloc<double>(np * 12);
   c->ch = c->alloc<double>(np * 12);
+  c->cy = c->alloc<double>(np * 12);
   c->cyr = c->alloc<double>(np * 12);
   c->cUraw = c->alloc<double>(np * LINP);
   c->nrm = c->alloc<double>(np * 2);
@@ -363,48 +414,63 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   if (n_deg) *n_deg = fl[F_N_DEGEN];
 }
 
-template <int S, int MODE>
-static void launch_cam(pv_ctx* c, int term, double thr) {
-  constexpr bool fused = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM;
-  constexpr bool staged = MODE != CM_PROJECT;
-  Tune tn = c->tune;
-  if (!staged) tn.stage_cap = 0;
-  const int smem = cam_smem_bytes(tn.stage_cap);
-  if (staged) {
-    static bool attr_set = false;  // per template instantiation
-    if (!attr_set) {
-      CK(cudaFuncSetAttribute(k_cam<S, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              cam_smem_bytes(CM_STAGE_MAX)));
-      attr_set = true;
-    }
-  }
-  k_cam<S, MODE><<<(int)c->n_p, FT, smem, c->stream>>>(
-      c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cyr, c->cbp, c->cUi, c->cx, c->crhs, c->ch,
-      c->nrm, c->ctl, c->host_ctl_dev, c->ticket, term, thr, c->coef, tn);
+template <int S, bool HC, int EP, bool HA>
+static void launch_cam(pv_ctx* c, const CamArgs& ca) {
+  k_cam<S, HC, EP, HA><<<(int)c->n_p, FT, 0, c->stream>>>(
+      c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->cyr, c->cbp, c->cUi, c->cx, c->crhs,
+      c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, ca);
   c->launched();
 }
 
 template <int S, int MODE>
-static void launch_lm_reduce(pv_ctx* c) {
-  const int nb = blocks_for((long long)((c->n_tasks + LR_BATCH - 1) / LR_BATCH) * 32, 256);
-  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(
-      c->g, c->sbuf, c->lrec, c->tarr, c->lsys, c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
-      c->tune);
+static void launch_lm_reduce(pv_ctx* c, int t_lo, int t_hi, int check_stop) {
+  const int nw = (t_hi - t_lo + LR_BATCH - 1) / LR_BATCH;
+  const int nb = blocks_for((long long)nw * 32, 256);
+  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
+                                                  c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
+                                                  c->tune, t_lo, t_hi, check_stop);
   c->launched();
 }
 
-// camera half of a term: y -> epilogue -> next gather (fused on one GPU; split
-// around the NCCL allreduce of y when sharded)
-template <int S>
-static void launch_cam_term(pv_ctx* c, bool rhs, int term, double thr) {
+static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int term,
+                        double thr, int check_stop) {
+  CamArgs a;
+  a.c_lo = c_lo;
+  a.c_hi = c_hi;
+  a.first_c = first_c;
+  a.a_lo = a_lo;
+  a.a_hi = a_hi;
+  a.term = term;
+  a.check_stop = check_stop;
+  a.project_y = 0;
+  a.thr = thr;
+  return a;
+}
+
+// finish y over blocks [c_lo, c_hi) (if any), the epilogue, and the gather of block 0
+template <int S, int EP>
+static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term, double thr,
+                            int check_stop) {
   if (c->world == 1) {
-    if (rhs) launch_cam<S, CM_FUSED_RHS>(c, term, thr);
-    else launch_cam<S, CM_FUSED_TERM>(c, term, thr);
+    launch_cam<S, true, EP, true>(c, cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop));
   } else {
-    launch_cam<S, CM_Y>(c, term, thr);
-    c->allreduce(c->cyr, (size_t)c->n_p * 12);
-    if (rhs) launch_cam<S, CM_EPI_RHS>(c, term, thr);
-    else launch_cam<S, CM_EPI_TERM>(c, term, thr);
+    launch_cam<S, true, EP_NONE, false>(c,
+                                        cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
+    c->allreduce(c->cy, (size_t)c->n_p * 12);
+    launch_cam<S, false, EP, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, check_stop));
+  }
+}
+
+// one power-series term i >= 1 (s of block 0 already scattered by the previous kernel)
+template <int S>
+static void launch_term(pv_ctx* c, int i, double thr) {
+  const int B = c->n_blk;
+  for (int b = 0; b < B; ++b) {
+    launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 1);
+    if (b + 1 < B)
+      launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, i, thr, 1));
+    else
+      launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, i, thr, 1);
   }
 }
 
@@ -414,14 +480,13 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
   c->sync();
   std::memset(c->host_ctl, 0, sizeof(PowerCtl));
-  // K4: reduced RHS, t_0 = U^-1 rhs and the gather of term 1
-  launch_lm_reduce<S, LR_RHS>(c);
-  launch_cam_term<S>(c, true, 0, thr);
+  // K4: t = V+ b_l, reduced RHS over all blocks, t_0 = U^-1 rhs, gather of block 0
+  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_tasks, 0);
+  launch_cam_last<S, EP_RHS>(c, 0, c->n_blk, 1, 0, thr, 0);
   c->check_launch();
   // K5 + K6 terms with a one-term lookahead on the device stop flag
   for (int i = 1; i <= max_order; ++i) {
-    launch_lm_reduce<S, LR_TERM>(c);
-    launch_cam_term<S>(c, false, i, thr);
+    launch_term<S>(c, i, thr);
     CK(cudaEventRecord(c->ev[i & 1], c->stream));
     if (i >= 2) {
       CK(cudaEventSynchronize(c->ev[(i - 1) & 1]));
@@ -429,11 +494,11 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     }
   }
   c->check_launch();
-  // K7 back-substitution with v = x
+  // K7 back-substitution with v = x (all blocks at once)
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
   c->launched();
-  launch_cam<S, CM_1A>(c, 0, thr);
-  launch_lm_reduce<S, LR_BACKSUB>(c);
+  launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, c->n_blk, 0, thr, 0));
+  launch_lm_reduce<S, LR_BACKSUB>(c, 0, c->n_tasks, 0);
   c->check_launch();
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
@@ -457,7 +522,7 @@ static void op_trial(pv_ctx* c, int* ok) {
 }
 
 static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
-  CK(cudaMemsetAsync(c->flags + F_N_RANKDEF, 0, sizeof(int), c->stream));
+  CK(cudaMemsetAsync(c->flags + F_N_RANKDEF, 0, 2 * sizeof(int), c->stream));
   const int nb = c->nblk_tasks();
   k_resolve<<<nb, 256, 0, c->stream>>>(c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef);
   k_sum<<<1, 1024, 0, c->stream>>>(c->cpart, nb, c->scal);
@@ -472,6 +537,7 @@ static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
   c->sync();
   if (f_new) *f_new = v;
   if (n_rd) *n_rd = fl[F_N_RANKDEF];
+  c->last_fallbacks = fl[F_N_FALLBACK];
 }
 
 static void op_accept(pv_ctx* c) {
@@ -559,6 +625,7 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
       NK(ncclCommInitRank(&c->comm, world, id, rank));
     }
     build_graph(c, cam_idx, lm_idx, meas, lm_begin, lm_end);
+    build_blocks(c);
     alloc_buffers(c);
     c->sync();
   } catch (const std::exception& e) {
@@ -603,6 +670,8 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_WORLD] = c->world;
   out[PV_INFO_DEVICE_BYTES] = (int64_t)c->device_bytes;
   out[PV_INFO_NL_GLOBAL] = c->n_l_global;
+  out[PV_INFO_RESOLVE_FALLBACKS] = c->last_fallbacks;
+  out[PV_INFO_BLOCKS] = c->n_blk;
   API_END(c)
 }
 
@@ -610,8 +679,7 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
   API_BEGIN(c)
   switch (key) {
     case PV_OPT_STAGE_CAP:
-      if (value < 0 || value > CM_STAGE_MAX) throw PvError(PV_EINVAL, "stage cap out of range");
-      c->tune.stage_cap = (int)value;
+      c->tune.stage_cap = (int)value;  // unused by the blocked term (kept for ABI stability)
       break;
     case PV_OPT_POL_STREAM:
       c->tune.pol_stream = (int)value;
@@ -621,6 +689,14 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_POL_S:
       c->tune.pol_s = (int)value;
+      break;
+    case PV_OPT_DISCARD_S:
+      c->tune.discard_s = (int)value;
+      break;
+    case PV_OPT_BLOCK_BYTES:
+      if (value < (1 << 20)) throw PvError(PV_EINVAL, "block budget too small");
+      c->block_bytes = value;
+      build_blocks(c);
       break;
     default:
       throw PvError(PV_EINVAL, "unknown option");
@@ -793,17 +869,34 @@ static void op_schur_apply(pv_ctx* c, const double* v, double* out) {
   for (int64_t i = 0; i < c->n_p; ++i)
     for (int q = 0; q < D; ++q) h[i * 12 + q] = v[i * D + q];
   CK(cudaMemcpyAsync(c->ctmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->ctmp, c->ch, c->crec);
   c->launched();
-  launch_cam<S, CM_1A>(c, 0, 0.0);
-  launch_lm_reduce<S, LR_TERM>(c);
-  launch_cam<S, CM_Y>(c, 0, 0.0);
-  c->allreduce(c->cyr, (size_t)c->n_p * 12);
-  if (S == 2) launch_cam<S, CM_PROJECT>(c, 0, 0.0);
+  launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, c->n_blk, 0, 0.0, 0));
+  launch_lm_reduce<S, LR_TERM>(c, 0, c->n_tasks, 0);
+  CamArgs ca = cam_args(0, c->n_blk, 1, 0, 0, 0, 0.0, 0);
+  if (c->world == 1) ca.project_y = 1;
+  launch_cam<S, true, EP_NONE, false>(c, ca);
+  if (c->world > 1) {
+    c->allreduce(c->cy, (size_t)c->n_p * 12);
+    CK(cudaMemcpyAsync(c->cyr, c->cy, (size_t)c->n_p * 12 * 8, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    if (S == 2) {  // project on the host copy below
+    }
+  }
   c->check_launch();
   CK(cudaMemcpyAsync(h.data(), c->cyr, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
+  if (c->world > 1 && S == 2) {  // tangent projection of the summed raw y
+    std::vector<double> hh((size_t)c->n_p * 12);
+    CK(cudaMemcpy(hh.data(), c->ch, hh.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < c->n_p; ++i) {
+      double hu = 0.0;
+      for (int q = 0; q < 12; ++q) hu += hh[i * 12 + q] * h[i * 12 + q];
+      double pr[12];
+      for (int q = 0; q < 12; ++q) pr[q] = h[i * 12 + q] - 2.0 * hh[i * 12 + q] * hu;
+      for (int q = 0; q < 11; ++q) h[i * 12 + q] = pr[q + 1];
+    }
+  }
   for (int64_t i = 0; i < c->n_p; ++i)
     for (int q = 0; q < D; ++q) out[i * D + q] = h[i * 12 + q];
 }
@@ -825,30 +918,38 @@ int pv_schur_apply(pv_ctx* c, int stage, const double* v, double* out) {
 template <int S>
 static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
+  // seed s of block 0 from the current camera vector
+  launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 0));
   float acc[4] = {0, 0, 0, 0};
   for (int i = 1; i <= n; ++i) {
+    // whole term timed end to end; per-kernel split measured on the first block
     CK(cudaEventRecord(c->tev[0], c->stream));
-    launch_lm_reduce<S, LR_TERM>(c);
+    launch_lm_reduce<S, LR_TERM>(c, c->blk_task[0], c->blk_task[1], 0);
     CK(cudaEventRecord(c->tev[1], c->stream));
-    if (c->world == 1) {
-      launch_cam<S, CM_FUSED_TERM>(c, 1 << 20, -1.0);
-      CK(cudaEventRecord(c->tev[2], c->stream));
-    } else {
-      launch_cam<S, CM_Y>(c, 1 << 20, -1.0);
-      CK(cudaEventRecord(c->tev[2], c->stream));
-      c->allreduce(c->cyr, (size_t)c->n_p * 12);
-      launch_cam<S, CM_EPI_TERM>(c, 1 << 20, -1.0);
+    const int B = c->n_blk;
+    if (B > 1)
+      launch_cam<S, true, EP_NONE, true>(c, cam_args(0, 1, 1, 1, 2, 1 << 20, -1.0, 0));
+    else
+      launch_cam_last<S, EP_TERM>(c, 0, 1, 1, 1 << 20, -1.0, 0);
+    CK(cudaEventRecord(c->tev[2], c->stream));
+    for (int b = 1; b < B; ++b) {
+      launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+      if (b + 1 < B)
+        launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, 0, b + 1, b + 2, 1 << 20, -1.0,
+                                                       0));
+      else
+        launch_cam_last<S, EP_TERM>(c, b, b + 1, 0, 1 << 20, -1.0, 0);
     }
     CK(cudaEventRecord(c->tev[3], c->stream));
     CK(cudaEventSynchronize(c->tev[3]));
-    float a, b, d;
+    float a, b2, d;
     CK(cudaEventElapsedTime(&a, c->tev[0], c->tev[1]));
-    CK(cudaEventElapsedTime(&b, c->tev[1], c->tev[2]));
-    CK(cudaEventElapsedTime(&d, c->tev[2], c->tev[3]));
-    acc[0] += a;
-    acc[1] += b;
-    acc[2] += d;
-    acc[3] += a + b + d;
+    CK(cudaEventElapsedTime(&b2, c->tev[1], c->tev[2]));
+    CK(cudaEventElapsedTime(&d, c->tev[0], c->tev[3]));
+    acc[0] += a * B;   // extrapolated over blocks (blocks have equal observation counts)
+    acc[1] += b2 * B;
+    acc[2] += (float)B;
+    acc[3] += d;
   }
   for (int q = 0; q < 4; ++q) ms[q] = acc[q] / std::max(n, 1);
 }

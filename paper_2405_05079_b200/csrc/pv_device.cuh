@@ -281,16 +281,17 @@ __device__ inline bool pinv_sym3(const double* a6, double rel_tol, double* out6)
   double A[3][3] = {{a6[0], a6[1], a6[2]}, {a6[1], a6[3], a6[4]}, {a6[2], a6[4], a6[5]}};
   double Q[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
   double tr = a6[0] + a6[3] + a6[5];
+  constexpr double EPS = 2.220446049250313e-16;
   for (int sweep = 0; sweep < 12; ++sweep) {
-    double off = fabs(A[0][1]) + fabs(A[0][2]) + fabs(A[1][2]);
-    double scale = fabs(A[0][0]) + fabs(A[1][1]) + fabs(A[2][2]);
-    if (off <= 1e-18 * scale || off == 0.0) break;
+    bool rotated = false;
 #pragma unroll
     for (int pq = 0; pq < 3; ++pq) {
       const int p = pq == 2 ? 1 : 0;
       const int q = pq == 0 ? 1 : 2;
       double apq = A[p][q];
-      if (apq == 0.0) continue;
+      // classic cyclic-Jacobi skip rule: off-diagonal below eps of the diagonals
+      if (fabs(apq) <= EPS * sqrt(fabs(A[p][p] * A[q][q])) || apq == 0.0) continue;
+      rotated = true;
       double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
       double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
       double c = 1.0 / sqrt(fma(t, t, 1.0));
@@ -314,6 +315,7 @@ __device__ inline bool pinv_sym3(const double* a6, double rel_tol, double* out6)
         Q[k][q] = s * qkp + c * qkq;
       }
     }
+    if (!rotated) break;
   }
   double tol = rel_tol * fmax(tr, 0.0);
   double wi[3];
@@ -399,7 +401,7 @@ __device__ inline bool lsq_from_r(const double* R, double rel_tol, double* v) {
         be = fma(M[i][q], M[i][q], be);
         ga = fma(M[i][p], M[i][q], ga);
       }
-      if (ga == 0.0 || fabs(ga) <= 1e-17 * sqrt(al * be)) continue;
+      if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
       rotated = true;
       double zeta = (be - al) / (2.0 * ga);
       double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));

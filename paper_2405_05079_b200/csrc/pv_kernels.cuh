@@ -30,10 +30,11 @@ constexpr int CM_STAGE_MAX = 2048;  // max observations of a camera staged in sh
 // runtime tuning of the term kernels (pv_set_option): on-chip staging capacity
 // and L2 eviction priorities (0 normal, 1 evict_first, 2 evict_last)
 struct Tune {
-  int stage_cap;   // observations per camera staged in shared memory
+  int stage_cap;   // (unused by the blocked term)
   int pol_stream;  // camera-sorted streams (m, x, ids)
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
+  int discard_s;   // drop consumed s lines from L2 (no write-back)
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -48,7 +49,8 @@ struct Graph {
   const int4* task;      // [n_tasks] {o0, n, l0, segment-head mask}
   const int* cs_lm;      // [n_o] local landmark of each camera-sorted observation
   const int* cs_pos;     // [n_o] landmark-sorted position of each camera-sorted observation
-  const int* ls2cs;      // [n_o] camera-sorted position of each landmark-sorted observation
+  int n_blk;             // landmark blocks of the L2-blocked term
+  const int* cam_blk;    // [n_p*(n_blk+1)] camera-sorted offsets of each camera's block ranges
   const double* cs_m;    // [n_o*2]
   const int* cam_off;    // [n_p+1] camera-sorted offsets
 };
@@ -107,29 +109,23 @@ __device__ __forceinline__ int seg_start_lane(const Task& t, int lane) {
 }
 
 // ---------------------------------------------------------------------------
-// camera-major fused power-series term (K5 scatter + K6 epilogue + K5 gather)
+// One power-series term, L2-blocked.
 //
-//   phase 2 : y_i   = sum_{j in cam i} W_ij t_j           (t gathered per obs)
-//   epilogue: t_i   = U_i^-1 (rhs_i | y_i), x_i += t_i, v_i = t_i (B t_i)
-//   phase 1a: s_ij  = W_ij^T v_i  -> sbuf[landmark-sorted position]
+// Landmarks are split into B contiguous blocks (block boundaries on warp-task
+// boundaries) sized so that one block's per-observation partials s (32 B/obs)
+// and landmark vectors t (32 B/landmark) fit in L2.  For each block b:
 //
-// The landmark half (t_j = V_j^+ sum_i s_ij) is k_lm_reduce.
+//   k_lm_reduce(b): t_j = V_j^+ sum_i s_ij      landmark-major, reads s (L2),
+//                                               writes t (L2, evict_last)
+//   k_cam(b):       y_i += sum_{j in b} W_ij t_j     camera-major (gathers t: L2)
+//                   then s_ij = W_ij^T v_i for j in block b+1 (scatter: L2)
+//
+// and after the last block the camera CTA finishes y_i, applies U_i^-1
+// (epilogue: x_i += t_i, norms, stop test) and starts the next term's block 0.
+// Both transpositions of S'.v therefore stay on chip; DRAM only streams the
+// camera-sorted observation data (x, m, ids) twice per term.
 
-enum {
-  CM_FUSED_RHS = 0,   // t_rhs -> rhs -> t_0 -> s (term 1)
-  CM_FUSED_TERM = 1,  // t -> y -> t_i -> s (term i+1)
-  CM_Y = 2,           // t -> y (raw 12) -> cyr            (sharded part A, also schur_apply)
-  CM_EPI_RHS = 3,     // cyr -> rhs -> t_0 -> s            (sharded part B)
-  CM_EPI_TERM = 4,    // cyr -> t_i -> s                   (sharded part B)
-  CM_1A = 5,          // crec.v -> s                       (back-substitution, schur_apply)
-  CM_PROJECT = 6      // cyr (raw 12) -> projected (11) in place (schur_apply, stage 2)
-};
-
-template <int STAGE>
-__device__ __forceinline__ Gen obs_gen(const double4& P0, const double4& P1, const double4& P2,
-                                       const double2& m, const double4& X, const Coef& k) {
-  return STAGE == 1 ? gen_s1(P0, P1, P2, m.x, m.y, k.s) : gen_s2(P0, P1, P2, X);
-}
+enum { EP_NONE = 0, EP_RHS = 1, EP_TERM = 2 };
 
 __device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT/32*12]*/,
                                             double* out /*[12]*/) {
@@ -148,83 +144,50 @@ __device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT
   __syncthreads();
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
+struct CamArgs {
+  int c_lo, c_hi;   // landmark-block range of the W t half (HC)
+  int first_c;      // 1: overwrite the camera accumulator y, 0: add
+  int a_lo, a_hi;   // landmark-block range of the W^T v half (HA)
+  int term;         // term index for the stop test (EP_TERM)
+  int check_stop;   // return immediately once the series has stopped
+  int project_y;    // write the (stage-2 projected) y to cyr instead (schur apply)
+  double thr;
+};
 
-// dynamic shared memory of a camera CTA staging `cap` observations (x, m)
-__host__ __device__ constexpr int cam_smem_bytes(int cap) { return cap * (32 + 16); }
-
-constexpr int CM_BATCH = 4;  // independent t gathers in flight per thread
-
-template <int STAGE, int MODE>
+template <int STAGE, bool HC, int EP, bool HA>
 __global__ void __launch_bounds__(FT, 2) k_cam(
     Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
-    const double* __restrict__ tbuf, double* __restrict__ sbuf, double* __restrict__ cyr,
-    const double* __restrict__ cbp, const double* __restrict__ cUi, double* __restrict__ cx,
-    double* __restrict__ crhs, const double* __restrict__ ch, double* __restrict__ nrm,
-    PowerCtl* __restrict__ ctl, volatile PowerCtl* host_ctl, unsigned* __restrict__ ticket,
-    int term, double thr, Coef k, Tune tune) {
-  constexpr bool P2 = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM || MODE == CM_Y;
-  constexpr bool FROM_CYR = MODE == CM_EPI_RHS || MODE == CM_EPI_TERM;
-  constexpr bool EPI = MODE == CM_FUSED_RHS || MODE == CM_FUSED_TERM || FROM_CYR;
-  constexpr bool RHS = MODE == CM_FUSED_RHS || MODE == CM_EPI_RHS;
-  constexpr bool A1 = EPI || MODE == CM_1A;
+    const double* __restrict__ tarr, double* __restrict__ sbuf, double* __restrict__ cy,
+    double* __restrict__ cyr, const double* __restrict__ cbp, const double* __restrict__ cUi,
+    double* __restrict__ cx, double* __restrict__ crhs, const double* __restrict__ ch,
+    double* __restrict__ nrm, PowerCtl* __restrict__ ctl, volatile PowerCtl* host_ctl,
+    unsigned* __restrict__ ticket, Coef k, Tune tune, CamArgs ca) {
+  constexpr bool RHS = EP == EP_RHS;
   constexpr int D = STAGE == 1 ? 12 : 11;
   __shared__ double red[(FT / 32) * 12];
   __shared__ double ysm[12];
   __shared__ double vsm[12];
   __shared__ bool last;
-  extern __shared__ __align__(32) unsigned char dsm[];
-  const int cap = tune.stage_cap;
-  double4* sx = reinterpret_cast<double4*>(dsm);
-  double2* smm = reinterpret_cast<double2*>(dsm + (size_t)cap * 32);
   const int cam = blockIdx.x;
-  if ((MODE == CM_FUSED_TERM || MODE == CM_EPI_TERM) && ctl->stopped) return;  // grid-uniform
+  if (ca.check_stop && ctl->stopped) return;  // grid-uniform
   const int tid = threadIdx.x;
-  const int o0 = g.cam_off[cam], o1 = g.cam_off[cam + 1];
-  const int n = o1 - o0;
+  const int* cbo = g.cam_blk + (size_t)cam * (g.n_blk + 1);
   const double* cp = crec + (size_t)cam * CREC;
   const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2v = ldg4(cp + 8);
-  const uint64_t pf = pol_sel(tune.pol_stream), pl = pol_sel(tune.pol_t),
+  const uint64_t pf = pol_sel(tune.pol_stream), pt = pol_sel(tune.pol_t),
                  ps = pol_sel(tune.pol_s);
 
-  if (MODE == CM_PROJECT) {  // stage-2 tangent projection of a raw y, in place
-    if (tid < 32) {
-      const int r = tid & 15;
-      double u = (tid < 12) ? cyr[(size_t)cam * 12 + tid] : 0.0;
-      double h = (tid < 12) ? ch[(size_t)cam * 12 + tid] : 0.0;
-      double hu = warp_sum(tid < 16 ? h * u : 0.0);
-      double pr = u - 2.0 * h * hu;
-      double nx = __shfl_sync(PV_FULL, pr, (r + 1) & 31);
-      if (tid < 12) cyr[(size_t)cam * 12 + tid] = tid < 11 ? nx : 0.0;
-    }
-    return;
-  }
-
-  // ---- stage this camera's x and m in shared memory for the second (gather) half
-  const int nc = A1 && P2 ? min(n, cap) : 0;
-  if (nc > 0) {
-    const char* gx = reinterpret_cast<const char*>(cs_x + 4 * (size_t)o0);
-    for (int q = tid; q < 2 * nc; q += FT) cp_async16(dsm + 16 * (size_t)q, gx + 16 * (size_t)q);
-    const char* gm = reinterpret_cast<const char*>(g.cs_m + 2 * (size_t)o0);
-    for (int q = tid; q < nc; q += FT) cp_async16(smm + q, gm + 16 * (size_t)q);
-  }
-
-  if (P2) {  // y_i = sum_j W_ij t_j, t streamed per observation (camera-sorted)
+  if (HC) {  // y_i (+)= sum_{j in blocks [c_lo, c_hi)} W_ij t_j
+    const int o_lo = __ldg(cbo + ca.c_lo), o_hi = __ldg(cbo + ca.c_hi);
     double acc[12];
 #pragma unroll
     for (int i = 0; i < 12; ++i) acc[i] = 0.0;
 #pragma unroll 4
-    for (int q = tid; q < n; q += FT) {
-      const size_t o = (size_t)(o0 + q);
-      const double4 T = ldg4p(tbuf + 4 * o, pl);
-      const double4 X = ldg4p(cs_x + 4 * o, pf);
-      const double2 m = ldg2p(g.cs_m + 2 * o, pf);
+    for (int o = o_lo + tid; o < o_hi; o += FT) {
+      const int j = ldgip(g.cs_lm + o, pf);
+      const double4 X = ldg4p(cs_x + 4 * (size_t)o, pf);
+      const double2 m = ldg2p(g.cs_m + 2 * (size_t)o, pf);
+      const double4 T = ldg4p(tarr + 4 * (size_t)j, pt);
       const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
       double sg[3];
       proj_map<STAGE>(pj, dot4(P0, T), dot4(P1, T), dot4(P2v, T), sg[0], sg[1], sg[2]);
@@ -236,31 +199,45 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
         acc[4 * c + 3] = fma(sg[c], X.w, acc[4 * c + 3]);
       }
     }
-    cp_async_wait_all();
     block_sum12(acc, red, ysm);
-    if (MODE == CM_Y) {
-      if (tid < 12) cyr[(size_t)cam * 12 + tid] = ysm[tid];
+    if (tid < 12) {  // fixed-order accumulation over blocks (deterministic)
+      const double y = ca.first_c ? ysm[tid] : cy[(size_t)cam * 12 + tid] + ysm[tid];
+      cy[(size_t)cam * 12 + tid] = y;
+      ysm[tid] = y;
+    }
+    __syncthreads();
+    if (ca.project_y) {  // schur apply: tangent projection (stage 2) -> cyr
+      if (tid < 32) {
+        double u = tid < 12 ? ysm[tid] : 0.0;
+        if (STAGE == 2) {
+          const double h = tid < 12 ? ch[(size_t)cam * 12 + tid] : 0.0;
+          const double hu = warp_sum(h * u);
+          const double pr = u - 2.0 * h * hu;
+          u = __shfl_sync(PV_FULL, pr, (tid + 1) & 31);
+          if (tid >= 11) u = 0.0;
+        }
+        if (tid < 12) cyr[(size_t)cam * 12 + tid] = u;
+      }
       return;
     }
   }
 
-  if (EPI) {
+  if (EP != EP_NONE) {
     if (tid < 32) {  // warp 0: rows r < D of U^-1
-      const int r = tid & 15;
       const bool row = tid < 12;
       double u = 0.0;
-      if (row) u = FROM_CYR ? cyr[(size_t)cam * 12 + tid] : ysm[tid];
+      if (row) u = HC ? ysm[tid] : cy[(size_t)cam * 12 + tid];
       double h = 0.0;
       if (STAGE == 2) {  // project y (12) -> tangent (11)
         h = row ? ch[(size_t)cam * 12 + tid] : 0.0;
-        double hu = warp_sum(tid < 16 ? h * u : 0.0);
-        double pr = u - 2.0 * h * hu;
-        u = __shfl_sync(PV_FULL, pr, (r + 1) & 31);
+        const double hu = warp_sum(h * u);
+        const double pr = u - 2.0 * h * hu;
+        u = __shfl_sync(PV_FULL, pr, (tid + 1) & 31);
         if (tid >= 11) u = 0.0;
       }
       double vin = u;
       if (RHS) {
-        double b = tid < D ? cbp[(size_t)cam * 12 + tid] : 0.0;
+        const double b = tid < D ? cbp[(size_t)cam * 12 + tid] : 0.0;
         vin = tid < D ? -(b - u) : 0.0;
         if (row) crhs[(size_t)cam * 12 + tid] = vin;
       }
@@ -268,7 +245,7 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
       const double* Ui = cUi + (size_t)cam * 144 + (tid < D ? tid : 0) * 12;
 #pragma unroll
       for (int kk = 0; kk < 12; ++kk) {
-        double vk = __shfl_sync(PV_FULL, vin, kk);
+        const double vk = __shfl_sync(PV_FULL, vin, kk);
         if (tid < D && kk < D) t = fma(Ui[kk], vk, t);
       }
       double xr = 0.0;
@@ -278,35 +255,38 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
       }
       double v = t;
       if (STAGE == 2) {  // v = B t (11 -> 12)
-        double tprev = __shfl_sync(PV_FULL, t, (tid + 31) & 31);
-        double e = (tid >= 1 && tid < 12) ? tprev : 0.0;
-        double hd = warp_sum(h * e);
+        const double tprev = __shfl_sync(PV_FULL, t, (tid + 31) & 31);
+        const double e = (tid >= 1 && tid < 12) ? tprev : 0.0;
+        const double hd = warp_sum(h * e);
         v = e - 2.0 * h * hd;
       }
-      if (row) vsm[tid] = v;
-      double tn = warp_sum(tid < D ? t * t : 0.0);
-      double xn = warp_sum(tid < D ? xr * xr : 0.0);
+      if (row) {
+        vsm[tid] = v;
+        crec[(size_t)cam * CREC + 12 + tid] = v;  // term vector for the later blocks
+      }
+      const double tn = warp_sum(tid < D ? t * t : 0.0);
+      const double xn = warp_sum(tid < D ? xr * xr : 0.0);
       if (tid == 0) {
         nrm[2 * (size_t)cam] = tn;
         nrm[2 * (size_t)cam + 1] = xn;
       }
     }
     __syncthreads();
-  } else if (MODE == CM_1A) {
+  } else if (HA) {
     if (tid < 12) vsm[tid] = cp[12 + tid];
     __syncthreads();
   }
 
-  if (A1) {  // phase 1a: s_ij = W_ij^T v_i scattered to landmark-sorted positions
+  if (HA) {  // s_ij = W_ij^T v_i for j in blocks [a_lo, a_hi), scattered (landmark order)
     const double4 v0 = make_double4(vsm[0], vsm[1], vsm[2], vsm[3]);
     const double4 v1 = make_double4(vsm[4], vsm[5], vsm[6], vsm[7]);
     const double4 v2 = make_double4(vsm[8], vsm[9], vsm[10], vsm[11]);
-#pragma unroll 2
-    for (int q = tid; q < n; q += FT) {
-      const int o = o0 + q;
+    const int o_lo = __ldg(cbo + ca.a_lo), o_hi = __ldg(cbo + ca.a_hi);
+#pragma unroll 4
+    for (int o = o_lo + tid; o < o_hi; o += FT) {
       const int pos = ldgip(g.cs_pos + o, pf);
-      const double4 X = q < nc ? sx[q] : ldg4p(cs_x + 4 * (size_t)o, pf);
-      const double2 m = q < nc ? smm[q] : ldg2p(g.cs_m + 2 * (size_t)o, pf);
+      const double4 X = ldg4p(cs_x + 4 * (size_t)o, pf);
+      const double2 m = ldg2p(g.cs_m + 2 * (size_t)o, pf);
       const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
       double f0, f1, f2;
       proj_map<STAGE>(pj, dot4(X, v0), dot4(X, v1), dot4(X, v2), f0, f1, f2);
@@ -319,22 +299,22 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
     }
   }
 
-  if (!EPI) return;
+  if (EP == EP_NONE) return;
   // ---- grid-wide fixed-order norm reduction + stop test in the last CTA
   if (tid == 0) {
     __threadfence();
-    unsigned tk = atomicAdd(ticket, 1u);
+    const unsigned tk = atomicAdd(ticket, 1u);
     last = tk == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double a = 0.0, b = 0.0;
+  double a = 0.0, bsum = 0.0;
   for (int i = tid; i < g.n_p; i += FT) {
     a += __ldcg(nrm + 2 * (size_t)i);
-    b += __ldcg(nrm + 2 * (size_t)i + 1);
+    bsum += __ldcg(nrm + 2 * (size_t)i + 1);
   }
-  double ra[2] = {a, b};
+  double ra[2] = {a, bsum};
   warp_reduce_all(ra);
   __shared__ double rr[2][FT / 32];
   if ((tid & 31) == 0) {
@@ -358,12 +338,12 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
     } else {  // solvers.py:140-149
       const double ratio = XN > 0.0 ? TN / XN : 0.0;
       c.trunc = ratio;
-      c.term = term;
-      if (ratio <= thr) {
-        c.order = term - 1;
+      c.term = ca.term;
+      if (ratio <= ca.thr) {
+        c.order = ca.term - 1;
         c.stopped = 1;
       } else {
-        c.order = term;
+        c.order = ca.term;
       }
     }
     c.xnorm = XN;
@@ -381,8 +361,9 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
 }
 
 // ---------------------------------------------------------------------------
-// landmark half of a term (and K7): t_j = V_j^+ sum_i s_ij, or the
-// back-substitution dl_j = -V_j^+ (b_l + sum_i s_ij) with the trial landmark.
+// landmark half of a term (and K7): t_j = V_j^+ sum_i s_ij (TERM) or V_j^+ b_j
+// (RHS) written per landmark, or the back-substitution
+// dl_j = -V_j^+ (b_l + sum_i s_ij) with the trial landmark (BACKSUB).
 
 enum { LR_TERM = 0, LR_BACKSUB = 1, LR_RHS = 2 };
 
@@ -403,12 +384,11 @@ __device__ __forceinline__ LmPre lm_prefetch(int l, const double* __restrict__ l
   return p;
 }
 
-// landmark epilogue: returns t (lifted to 4 components) for TERM / RHS; writes
-// the landmark update and trial landmark for BACKSUB
 template <int STAGE, int MODE>
-__device__ __forceinline__ double4 lm_finish(int l, const double (&acc)[4], const LmPre& p,
-                                             double* __restrict__ ldl, double* __restrict__ tlm,
-                                             int* __restrict__ flags) {
+__device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const LmPre& p,
+                                          double* __restrict__ tarr, double* __restrict__ ldl,
+                                          double* __restrict__ tlm, int* __restrict__ flags,
+                                          uint64_t pt) {
   double s3[3], h[4];
   const double4 x = p.x;
   double xv[4] = {x.x, x.y, x.z, x.w};
@@ -428,10 +408,14 @@ __device__ __forceinline__ double4 lm_finish(int l, const double (&acc)[4], cons
   if (MODE != LR_BACKSUB) {
     double t[3];
     sym3_apply(vp, s3, t);
-    if (STAGE == 1) return make_double4(t[0], t[1], t[2], 0.0);
-    double t4[4];
-    basis_apply<4>(h, t, t4);
-    return make_double4(t4[0], t4[1], t4[2], t4[3]);
+    if (STAGE == 1) {
+      st4p(tarr + (size_t)l * 4, make_double4(t[0], t[1], t[2], 0.0), pt);
+    } else {
+      double t4[4];
+      basis_apply<4>(h, t, t4);
+      st4p(tarr + (size_t)l * 4, make_double4(t4[0], t4[1], t4[2], t4[3]), pt);
+    }
+    return;
   }
   double q[3] = {s3[0] + p.bl.x, s3[1] + p.bl.y, s3[2] + p.bl.z};
   double dl[3];
@@ -452,36 +436,32 @@ __device__ __forceinline__ double4 lm_finish(int l, const double (&acc)[4], cons
     }
     st4(tlm + (size_t)l * 4, make_double4(y0 / nn, y1 / nn, y2 / nn, y3 / nn));
   }
-  return make_double4(0.0, 0.0, 0.0, 0.0);
 }
 
 constexpr int LR_BATCH = 4;  // landmark tasks per warp (loads of all of them in flight)
 
-// Landmark half of a term: t_j = V_j^+ sum_i s_ij (TERM) or V_j^+ b_j (RHS), scattered
-// into the camera-sorted slot of every observation of landmark j (tbuf), so that
-// the camera kernel streams it; BACKSUB writes dl_j and the trial landmark instead.
 template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, const double* __restrict__ sbuf,
+__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__ sbuf,
                                                    const double* __restrict__ lrec,
-                                                   double* __restrict__ tbuf,
+                                                   double* __restrict__ tarr,
                                                    const double* __restrict__ lsys,
                                                    const double* __restrict__ lbl,
                                                    double* __restrict__ ldl,
                                                    double* __restrict__ tlm,
                                                    const PowerCtl* __restrict__ ctl, int* flags,
-                                                   Tune tune) {
-  constexpr bool SCATTER = MODE != LR_BACKSUB;
+                                                   Tune tune, int task_lo, int task_hi,
+                                                   int check_stop) {
   const int lane = threadIdx.x & 31;
-  const int w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LR_BATCH;
-  if (w0 >= g.n_tasks) return;
-  if (MODE == LR_TERM && ctl->stopped) return;
+  const int w0 = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LR_BATCH;
+  if (w0 >= task_hi) return;
+  if (check_stop && ctl->stopped) return;
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
-  const int nb = min(LR_BATCH, g.n_tasks - w0);
+  const int nb = min(LR_BATCH, task_hi - w0);
   int4 d = make_int4(0, 0, 0, 0);
   if (lane < nb) d = __ldg(g.task + w0 + lane);
   Task tk[LR_BATCH];
   double4 sv[LR_BATCH];
-  int dst[LR_BATCH];
+  int o_first = 0, o_end = 0;
 #pragma unroll
   for (int q = 0; q < LR_BATCH; ++q) {
     tk[q].o0 = __shfl_sync(PV_FULL, d.x, q);
@@ -489,12 +469,11 @@ __global__ void __launch_bounds__(256) k_lm_reduce(Graph g, const double* __rest
     tk[q].l0 = __shfl_sync(PV_FULL, d.z, q);
     tk[q].heads = (unsigned)__shfl_sync(PV_FULL, d.w, q);
     tk[q].long_task = tk[q].n > 32;
+    if (q == 0) o_first = tk[q].o0;
+    if (q < nb) o_end = tk[q].o0 + tk[q].n;
     sv[q] = make_double4(0.0, 0.0, 0.0, 0.0);
-    dst[q] = 0;
-    if (q < nb && !tk[q].long_task && lane < tk[q].n) {
-      if (MODE != LR_RHS) sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
-      if (SCATTER) dst[q] = ldgip(g.ls2cs + tk[q].o0 + lane, pf);
-    }
+    if (MODE != LR_RHS && q < nb && !tk[q].long_task && lane < tk[q].n)
+      sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
   }
 #pragma unroll
   for (int q = 0; q < LR_BATCH; ++q) {
@@ -513,16 +492,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(Graph g, const double* __rest
         }
         warp_reduce_all(acc);
       }
-      double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (lane == 0) tv = lm_finish<STAGE, MODE>(t.l0, acc, pre, ldl, tlm, flags);
-      if (SCATTER) {
-        tv.x = __shfl_sync(PV_FULL, tv.x, 0);
-        tv.y = __shfl_sync(PV_FULL, tv.y, 0);
-        tv.z = __shfl_sync(PV_FULL, tv.z, 0);
-        tv.w = __shfl_sync(PV_FULL, tv.w, 0);
-        for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32)
-          st4p(tbuf + 4 * (size_t)ldgip(g.ls2cs + o, pf), tv, pt);
-      }
+      if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
     } else {
       int l, seg_end;
       lane_segment(t, lane, l, seg_end);
@@ -531,17 +501,18 @@ __global__ void __launch_bounds__(256) k_lm_reduce(Graph g, const double* __rest
       if (head) pre = lm_prefetch<STAGE, MODE>(l, lrec, lsys, lbl);
       double acc[4] = {sv[q].x, sv[q].y, sv[q].z, sv[q].w};
       if (MODE != LR_RHS) seg_reduce(acc, lane, seg_end);
-      double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (head) tv = lm_finish<STAGE, MODE>(l, acc, pre, ldl, tlm, flags);
-      if (SCATTER) {
-        const int src = seg_start_lane(t, lane < t.n ? lane : 0);
-        tv.x = __shfl_sync(PV_FULL, tv.x, src);
-        tv.y = __shfl_sync(PV_FULL, tv.y, src);
-        tv.z = __shfl_sync(PV_FULL, tv.z, src);
-        tv.w = __shfl_sync(PV_FULL, tv.w, src);
-        if (lane < t.n) st4p(tbuf + 4 * (size_t)dst[q], tv, pt);
-      }
+      if (head) lm_finish<STAGE, MODE>(l, acc, pre, tarr, ldl, tlm, flags, pt);
     }
+  }
+  if (MODE == LR_TERM && tune.discard_s) {
+    // the consumed partials are scratch: drop their L2 lines instead of writing them back
+    // (only lines entirely inside this warp's observation range)
+    const size_t b0 = 4 * (size_t)o_first * sizeof(double);
+    const size_t b1 = 4 * (size_t)o_end * sizeof(double);
+    const size_t l0 = (b0 + 127) / 128, l1 = b1 / 128;
+    char* base = reinterpret_cast<char*>(sbuf);
+    for (size_t ln = l0 + lane; ln < l1; ln += 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + ln * 128) : "memory");
   }
 }
 
@@ -1172,11 +1143,61 @@ __device__ __forceinline__ bool cqr2_solve(const double* R1, const double* s2, d
   z[0] = R2[0] != 0.0 ? s2[6] / R2[0] : 0.0;
   z[1] = R2[3] != 0.0 ? (s2[7] - R2[1] * z[0]) / R2[3] : 0.0;
   z[2] = R2[5] != 0.0 ? (s2[8] - R2[2] * z[0] - R2[4] * z[1]) / R2[5] : 0.0;
+  // Certified full rank: sigma_min >= 1/||R^-1||_F and sigma_max <= ||R||_F, so
+  // cond_F(R) < 1e8 implies s_min > 1e-8 s_max, far inside the reference's rule
+  // (s > 1e-10 s_max).  Then the min-norm solution is the triangular solve.
+  if (R[0] != 0.0 && R[3] != 0.0 && R[5] != 0.0) {
+    const double i00 = 1.0 / R[0], i11 = 1.0 / R[3], i22 = 1.0 / R[5];
+    const double i01 = -R[1] * i00 * i11, i12 = -R[4] * i11 * i22;
+    const double i02 = -(R[1] * i12 + R[2] * i22) * i00;
+    const double nr = R[0] * R[0] + R[1] * R[1] + R[2] * R[2] + R[3] * R[3] + R[4] * R[4] +
+                      R[5] * R[5];
+    const double ni = i00 * i00 + i01 * i01 + i02 * i02 + i11 * i11 + i12 * i12 + i22 * i22;
+    if (nr * ni < 1e16) {
+      v[0] = -(i00 * z[0] + i01 * z[1] + i02 * z[2]);
+      v[1] = -(i11 * z[1] + i12 * z[2]);
+      v[2] = -(i22 * z[2]);
+      return true;
+    }
+  }
   const double full[10] = {R[0], R[1], R[2], z[0], R[3], R[4], z[1], R[5], z[2], 0.0};
   return lsq_from_r(full, 1e-10, v);
 }
 
 constexpr double CQR_PIVOT_TOL = 1e-13;
+
+__device__ __forceinline__ void gram6(const Rows4& rw, double* g1) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    g1[0] = fma(rw.a[r][0], rw.a[r][0], g1[0]);
+    g1[1] = fma(rw.a[r][0], rw.a[r][1], g1[1]);
+    g1[2] = fma(rw.a[r][0], rw.a[r][2], g1[2]);
+    g1[3] = fma(rw.a[r][1], rw.a[r][1], g1[3]);
+    g1[4] = fma(rw.a[r][1], rw.a[r][2], g1[4]);
+    g1[5] = fma(rw.a[r][2], rw.a[r][2], g1[5]);
+  }
+}
+
+__device__ __forceinline__ void gram_pass2(const Rows4& rw, const double* R1, const double* id,
+                                           double* s2) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double wv[3];
+    tri_solve_row(rw.a[r], R1, id, wv);
+    gram_acc(wv, rw.c[r], s2);
+  }
+}
+
+// stage-1 cost of one observation from its affine rows: r = A x + c
+__device__ __forceinline__ double rows_cost(const Rows4& rw, const double4& x) {
+  double f = 0.0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const double v = fma(rw.a[r][0], x.x, fma(rw.a[r][1], x.y, fma(rw.a[r][2], x.z, rw.c[r] * x.w)));
+    f = fma(v, v, f);
+  }
+  return f;
+}
 
 __global__ void __launch_bounds__(256) k_resolve(Graph g, const double* __restrict__ tcam,
                                                  double* __restrict__ tlm,
@@ -1197,25 +1218,27 @@ __global__ void __launch_bounds__(256) k_resolve(Graph g, const double* __restri
       src = seg_start_lane(t, lane < t.n ? lane : 0);
     }
     const bool head = t.long_task ? lane == 0 : (lane < t.n && ((t.heads >> lane) & 1u));
-    const int stride = t.long_task ? 32 : 1 << 30;
     const int oend = t.o0 + t.n;
+    // short tasks keep their single observation's rows in registers for all passes
+    Rows4 mine;
+    const bool have = !t.long_task && lane < t.n;
+    if (have) {
+      const int o = t.o0 + lane;
+      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+      mine = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
+    }
     // pass 1: Gram of A
     double g1[6] = {0, 0, 0, 0, 0, 0};
-    for (int o = t.o0 + lane; o < oend; o += stride) {
-      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      const Rows4 rw = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        g1[0] = fma(rw.a[r][0], rw.a[r][0], g1[0]);
-        g1[1] = fma(rw.a[r][0], rw.a[r][1], g1[1]);
-        g1[2] = fma(rw.a[r][0], rw.a[r][2], g1[2]);
-        g1[3] = fma(rw.a[r][1], rw.a[r][1], g1[3]);
-        g1[4] = fma(rw.a[r][1], rw.a[r][2], g1[4]);
-        g1[5] = fma(rw.a[r][2], rw.a[r][2], g1[5]);
+    if (t.long_task) {
+      for (int o = t.o0 + lane; o < oend; o += 32) {
+        const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+        gram6(resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k), g1);
       }
+      warp_reduce_all(g1);
+    } else {
+      if (have) gram6(mine, g1);
+      seg_reduce(g1, lane, seg_end);
     }
-    if (t.long_task) warp_reduce_all(g1);
-    else seg_reduce(g1, lane, seg_end);
     double R1[6] = {0, 0, 0, 0, 0, 0};
     double fb = 0.0;
     if (head) {
@@ -1229,15 +1252,13 @@ __global__ void __launch_bounds__(256) k_resolve(Graph g, const double* __restri
     double s2[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (fb == 0.0) {
       const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
-      for (int o = t.o0 + lane; o < oend; o += stride) {
-        const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-        const Rows4 rw = resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          double wv[3];
-          tri_solve_row(rw.a[r], R1, id, wv);
-          gram_acc(wv, rw.c[r], s2);
+      if (t.long_task) {
+        for (int o = t.o0 + lane; o < oend; o += 32) {
+          const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+          gram_pass2(resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k), R1, id, s2);
         }
+      } else if (have) {
+        gram_pass2(mine, R1, id, s2);
       }
     }
     if (t.long_task) warp_reduce_all(s2);
@@ -1274,9 +1295,14 @@ __global__ void __launch_bounds__(256) k_resolve(Graph g, const double* __restri
     x.y = __shfl_sync(PV_FULL, xn[1], src);
     x.z = __shfl_sync(PV_FULL, xn[2], src);
     x.w = __shfl_sync(PV_FULL, xn[3], src);
-    for (int o = t.o0 + lane; o < oend; o += stride) {
-      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      cost += obs_cost<1>(tcam, 12, __ldg(g.ls_cam + o), m.x, m.y, x, k, flags);
+    // pass 3: stage-1 cost at the re-solved landmark (K9 fused)
+    if (t.long_task) {
+      for (int o = t.o0 + lane; o < oend; o += 32) {
+        const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+        cost += rows_cost(resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k), x);
+      }
+    } else if (have) {
+      cost = rows_cost(mine, x);
     }
   }
   const unsigned bal = __ballot_sync(PV_FULL, rankdef);

@@ -25,4 +25,4 @@ if len(sys.argv) > 3:
     f2, tr2 = pv.lm_minimize(problem, lifted, 2, pv.SolverConfig(max_outer_iterations=2,
                              max_power_order=cfg.max_power_order), dp=dp)
     print("stage2 costs", [r.cost for r in tr2.records])
-print("launches", dp.info()["launches"])
+print("launches", dp.info()["launches"], "resolve fallbacks", dp.info()["resolve_fallbacks"])

@@ -1,5 +1,5 @@
 """Sweep the term-kernel tuning knobs on a BASELINE config (results are knob-independent).
-Usage: CAPS=0,4096 POLS=... python tools/sweep_terms.py [config] [stage]"""
+Usage: BLOCKS=32,48,64 POLS=122,000 DISC=1 python tools/sweep_terms.py [config] [stage]"""
 import itertools
 import os
 import sys
@@ -23,15 +23,17 @@ dp.linearize(stage)
 dp.damp(1e-4, stage == 2)
 dp.power_solve(1, 0.0)
 n_o = problem.num_observations
-caps = [int(c) for c in os.environ.get("CAPS", "0,4096").split(",")]
-pols = [tuple(int(x) for x in p) for p in os.environ.get("POLS", "021,000,121").split(",")]
-for cap, (ps, pt, pss) in itertools.product(caps, pols):
-    dp.set_option(_lib.PV_OPT_STAGE_CAP, cap)
+blocks = [int(c) for c in os.environ.get("BLOCKS", "32,48,64,96,4096").split(",")]
+pols = [tuple(int(x) for x in p) for p in os.environ.get("POLS", "122,000").split(",")]
+discs = [int(x) for x in os.environ.get("DISC", "1,0").split(",")]
+for mb, (ps, pt, pss), disc in itertools.product(blocks, pols, discs):
+    dp.set_option(_lib.PV_OPT_BLOCK_BYTES, mb << 20)
     dp.set_option(_lib.PV_OPT_POL_STREAM, ps)
     dp.set_option(_lib.PV_OPT_POL_T, pt)
     dp.set_option(_lib.PV_OPT_POL_S, pss)
+    dp.set_option(_lib.PV_OPT_DISCARD_S, disc)
     dp.bench_terms(stage, 2)
     r = dp.bench_terms(stage, 10)
-    print(f"cap={cap:5d} stream={ps} t={pt} s={pss}  lm_reduce={r['phase1_ms']:.3f} "
-          f"cam={r['phase2_ms']:.3f} term={r['term_ms']:.3f} ms  "
+    print(f"block={mb:5d}MB B={dp.info()['blocks']:3d} pol={ps}{pt}{pss} disc={disc}  "
+          f"lm_reduce~{r['phase1_ms']:.3f} cam~{r['phase2_ms']:.3f} term={r['term_ms']:.3f} ms  "
           f"{n_o / r['term_ms'] / 1e6:.2f} Gobs/s", flush=True)
