@@ -107,20 +107,33 @@ class ClockSampler:
 
 
 def term_bytes(n_p, n_l, n_o, stage=1):
-    """Algorithmic (compulsory) DRAM bytes of one power-series term per kernel.
+    """Algorithmic bytes of one power-series term per kernel.
 
-    DESIGN.md section 5: every array element a kernel must touch, counted once.
-    k_lm_reduce streams s (32 B/obs) and the landmark->camera-order map (4 B/obs),
-    scatters t into the camera-sorted slot of every observation (32 B/obs), and
-    per landmark reads the task descriptor, V+ (2 x 32 B sectors), b/x.  k_cam
-    streams the camera-sorted t (32), x (32), m (16), landmark-sorted position
-    (4) and scatters s (32) per observation, plus per camera P, U^-1 and the
-    small vectors (~1.6 KB).
+    Every array element a kernel must touch, counted once per pass.  k_cam
+    (summed over the landmark blocks) streams the camera-sorted x (32), m (16)
+    and one id (4) twice -- once for W t, once for W^T v -- scatters s (32) and
+    reads each landmark's t once (32 per landmark), plus per camera P, U^-1 and
+    the small vectors (~1.6 KB).  k_lm_reduce reads s (32 per observation) and
+    per landmark the task descriptor, V+ (2 x 32 B sectors), x (stage 2) and
+    writes t (32).  s and t are sized per block to stay in the persisting L2,
+    so the DRAM-compulsory part is the streams + per-landmark data.
     """
-    lmr = 36 * n_o + 32 * n_o + (104 if stage == 1 else 136) * n_l
-    cam = 116 * n_o + 1600 * n_p
+    lmr = 32 * n_o + (104 if stage == 1 else 136) * n_l
+    cam = 136 * n_o + 32 * n_l + 1600 * n_p
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
     return {"lm_reduce": lmr, "cam": cam, "r1_term": r1}
+
+
+def traffic_from_profile(kernel, n_o):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture (vlarge only)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        if t.get("n_obs") == n_o:
+            return t["per_term_bytes"].get(kernel)
+    except Exception:
+        pass
+    return None
 
 
 def cpu_port_lm(fraction, iters=2, seed=0):
@@ -291,8 +304,10 @@ def main():
             "r1_equivalent_frac_of_8tbs": tb["r1_term"] * world / (term_ms * 1e-3) / 8e12,
             "kernels": kern}
     roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak,
-                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": None, "kernel": dom,
-                "peak_source": peak_src}
+                "unit": "GB/s", "frac": kern[dom]["frac"],
+                "traffic": traffic_from_profile(dom, n_o), "kernel": dom,
+                "peak_source": peak_src,
+                "note": "achieved/traffic per term (summed over the landmark-block launches)"}
 
     # ---- stage 2 (RiPoBA) iteration throughput from the lifted state ------------
     stage2 = None

@@ -67,12 +67,14 @@ struct pv_ctx {
   // graph (device)
   Graph g{};
   int *d_ls_cam = nullptr, *d_lm_off = nullptr, *d_task_lm = nullptr, *d_cs_lm = nullptr,
-      *d_cs_pos = nullptr, *d_cam_off = nullptr, *d_cam_blk = nullptr;
+      *d_cs_pos = nullptr, *d_seg = nullptr;
   // host copies kept for re-blocking (pv_set_option PV_OPT_BLOCK_BYTES)
-  std::vector<int> h_cs_lm, h_cam_off, h_task_desc;
+  std::vector<int> h_ls_cam, h_ls_lid, h_task_desc;
   std::vector<int> blk_task;  // [n_blk+1] task boundaries of the landmark blocks
   int n_blk = 1;
-  int64_t block_bytes = 48ll << 20;
+  int64_t block_bytes = 80ll << 20;
+  size_t seg_bytes = 0;
+  int64_t persist_l2 = 0;
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
@@ -172,22 +174,6 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
       ls_m[2 * p + 1] = meas[2 * o + 1];
     }
   }
-  // camera-sorted permutation of the landmark-sorted rows
-  std::vector<int> cam_off(n_p + 1, 0);
-  for (int64_t k = 0; k < n_os; ++k) cam_off[ls_cam[k] + 1]++;
-  for (int64_t i = 0; i < n_p; ++i) cam_off[i + 1] += cam_off[i];
-  std::vector<int> cs_lm(n_os), cs_pos(n_os);
-  std::vector<double> cs_m(2 * n_os);
-  {
-    std::vector<int> pos(cam_off.begin(), cam_off.end() - 1);
-    for (int64_t k = 0; k < n_os; ++k) {
-      int p = pos[ls_cam[k]]++;
-      cs_lm[p] = ls_lid[k];
-      cs_pos[p] = (int)k;
-      cs_m[2 * p] = ls_m[2 * k];
-      cs_m[2 * p + 1] = ls_m[2 * k + 1];
-    }
-  }
   // landmark tasks: whole landmarks packed into <= 32 lanes, or one long landmark;
   // descriptor {first obs, obs count, first landmark, segment-head lane mask}
   std::vector<int> task_desc;
@@ -236,15 +222,14 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->d_ls_m = up_d(ls_m);
   c->d_lm_off = up_i(lm_off);
   c->d_task_lm = up_i(task_desc);
-  cs_lm.resize(cs_lm.size() + 8, 0);
-  cs_pos.resize(cs_pos.size() + 8, 0);
-  c->d_cs_lm = up_i(cs_lm);
-  c->d_cs_m = up_d(cs_m);
-  c->d_cs_pos = up_i(cs_pos);
-  c->d_cam_off = up_i(cam_off);
+  // camera-sorted arrays are (re)built by build_blocks in block-major order
+  // padded by one staging chunk (k_cam copies whole chunks)
+  c->d_cs_lm = c->alloc<int>((size_t)n_os + 128);
+  c->d_cs_pos = c->alloc<int>((size_t)n_os + 128);
+  c->d_cs_m = c->alloc<double>(2 * ((size_t)n_os + 128));
   c->sync();  // host vectors go out of scope
-  c->h_cs_lm.assign(cs_lm.begin(), cs_lm.begin() + n_os);
-  c->h_cam_off = cam_off;
+  c->h_ls_cam = std::move(ls_cam);
+  c->h_ls_lid = std::move(ls_lid);
   c->h_task_desc = task_desc;
 
   Graph& g = c->g;
@@ -259,7 +244,6 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   g.cs_lm = c->d_cs_lm;
   g.cs_m = c->d_cs_m;
   g.cs_pos = c->d_cs_pos;
-  g.cam_off = c->d_cam_off;
 }
 
 // Landmark blocks of the L2-blocked term: contiguous task ranges with ~equal
@@ -267,6 +251,7 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
 // budget; per camera, the camera-sorted sub-range of each block.
 static void build_blocks(pv_ctx* c) {
   const int n_os = c->n_os, n_tasks = c->n_tasks;
+  const int64_t n_p = c->n_p;
   const int64_t want = std::max<int64_t>(1, ((int64_t)n_os * 32 + c->block_bytes - 1) /
                                                 std::max<int64_t>(c->block_bytes, 1));
   const int nb = (int)std::min<int64_t>(want, std::max(1, n_tasks));
@@ -279,31 +264,56 @@ static void build_blocks(pv_ctx* c) {
   }
   bt.push_back(n_tasks);
   const int B = (int)bt.size() - 1;
-  std::vector<int> lm_first(B + 1);
-  for (int b = 0; b < B; ++b) lm_first[b] = n_tasks ? c->h_task_desc[4 * bt[b] + 2] : 0;
-  lm_first[B] = c->n_ls;
-  std::vector<int> cb((size_t)c->n_p * (B + 1));
-  for (int64_t cam = 0; cam < c->n_p; ++cam) {
-    const int o0 = c->h_cam_off[cam], o1 = c->h_cam_off[cam + 1];
-    int o = o0;
-    for (int b = 0; b <= B; ++b) {
-      while (o < o1 && c->h_cs_lm[o] < lm_first[b]) ++o;
-      cb[(size_t)cam * (B + 1) + b] = (b == B) ? o1 : o;
+  // block of every landmark-sorted observation (blocks are contiguous in ls order)
+  std::vector<int> obs_blk_end(B);
+  for (int b = 0; b < B; ++b) {
+    const int t1 = bt[b + 1];
+    obs_blk_end[b] = t1 < n_tasks ? c->h_task_desc[4 * t1] : n_os;
+  }
+  // block-major camera-sorted order: stable counting sort of ls rows by (block, camera)
+  std::vector<int> seg((size_t)B * n_p + 1, 0);
+  {
+    int b = 0;
+    for (int k = 0; k < n_os; ++k) {
+      while (k >= obs_blk_end[b]) ++b;
+      seg[(size_t)b * n_p + c->h_ls_cam[k] + 1]++;
+    }
+    for (size_t i = 0; i + 1 < seg.size(); ++i) seg[i + 1] += seg[i];
+  }
+  std::vector<int> cs_lm((size_t)n_os + 128, 0), cs_pos((size_t)n_os + 128, 0);
+  {
+    std::vector<int> pos(seg.begin(), seg.end() - 1);
+    int b = 0;
+    for (int k = 0; k < n_os; ++k) {
+      while (k >= obs_blk_end[b]) ++b;
+      const int p = pos[(size_t)b * n_p + c->h_ls_cam[k]]++;
+      cs_lm[p] = c->h_ls_lid[k];
+      cs_pos[p] = k;
     }
   }
-  if (c->d_cam_blk) {
-    CK(cudaFree(c->d_cam_blk));
-    auto it = std::find(c->allocs.begin(), c->allocs.end(), (void*)c->d_cam_blk);
+  if (c->d_seg) {
+    CK(cudaFree(c->d_seg));
+    auto it = std::find(c->allocs.begin(), c->allocs.end(), (void*)c->d_seg);
     if (it != c->allocs.end()) c->allocs.erase(it);
+    c->device_bytes -= c->seg_bytes;
   }
-  c->d_cam_blk = c->alloc<int>(cb.size());
-  CK(cudaMemcpyAsync(c->d_cam_blk, cb.data(), cb.size() * sizeof(int), cudaMemcpyHostToDevice,
+  c->d_seg = c->alloc<int>(seg.size());
+  c->seg_bytes = seg.size() * sizeof(int);
+  CK(cudaMemcpyAsync(c->d_seg, seg.data(), seg.size() * sizeof(int), cudaMemcpyHostToDevice,
                      c->stream));
+  CK(cudaMemcpyAsync(c->d_cs_lm, cs_lm.data(), cs_lm.size() * sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_cs_pos, cs_pos.data(), cs_pos.size() * sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream));
+  k_gather_m<<<blocks_for(n_os, 256), 256, 0, c->stream>>>(n_os, c->d_cs_pos, c->d_ls_m,
+                                                           c->d_cs_m);
+  c->launched();
   c->sync();
   c->blk_task = bt;
   c->n_blk = B;
   c->g.n_blk = B;
-  c->g.cam_blk = c->d_cam_blk;
+  c->g.seg = c->d_seg;
+  c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -313,7 +323,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->lsys = c->alloc<double>(nl * LSYS);
   c->lvr = c->alloc<double>(nl * 8);
   c->tarr = c->alloc<double>(nl * 4);  // t per landmark
-  c->cs_x = c->alloc<double>((size_t)c->n_os * 4);
+  c->cs_x = c->alloc<double>(((size_t)c->n_os + 128) * 4);
   c->sbuf = c->alloc<double>((size_t)c->n_os * 4);
   c->lbl = c->alloc<double>(nl * 4);
   c->ldl = c->alloc<double>(nl * 4);
@@ -416,7 +426,13 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
 
 template <int S, bool HC, int EP, bool HA>
 static void launch_cam(pv_ctx* c, const CamArgs& ca) {
-  k_cam<S, HC, EP, HA><<<(int)c->n_p, FT, 0, c->stream>>>(
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            CAM_SMEM));
+    attr_set = true;
+  }
+  k_cam<S, HC, EP, HA><<<blocks_for(c->n_p * 32, 256), 256, CAM_SMEM, c->stream>>>(
       c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->cyr, c->cbp, c->cUi, c->cx, c->crhs,
       c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, ca);
   c->launched();
@@ -615,6 +631,17 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
     c->coef.s2 = std::sqrt(eta);
     c->coef.s = 1.0 - eta;
     CK(cudaSetDevice(device));
+    {
+      // evict_last (L2::cache_hint) lines live in the persisting L2 carve-out, which
+      // defaults to 0 bytes: reserve the maximum so a landmark block's partials stay on chip
+      int max_persist = 0;
+      CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+      size_t cur = 0;
+      CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      if (cur < (size_t)max_persist)
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist));
+      c->persist_l2 = max_persist;
+    }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->tev) CK(cudaEventCreate(&e));
@@ -672,6 +699,7 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_NL_GLOBAL] = c->n_l_global;
   out[PV_INFO_RESOLVE_FALLBACKS] = c->last_fallbacks;
   out[PV_INFO_BLOCKS] = c->n_blk;
+  out[PV_INFO_PERSIST_L2] = c->persist_l2;
   API_END(c)
 }
 

@@ -50,9 +50,9 @@ struct Graph {
   const int* cs_lm;      // [n_o] local landmark of each camera-sorted observation
   const int* cs_pos;     // [n_o] landmark-sorted position of each camera-sorted observation
   int n_blk;             // landmark blocks of the L2-blocked term
-  const int* cam_blk;    // [n_p*(n_blk+1)] camera-sorted offsets of each camera's block ranges
+  const int* seg;        // [n_blk*n_p+1] start of segment (block b, camera c) at b*n_p+c in the
+                         // block-major camera-sorted order (block, camera, landmark)
   const double* cs_m;    // [n_o*2]
-  const int* cam_off;    // [n_p+1] camera-sorted offsets
 };
 
 struct PowerCtl {
@@ -144,6 +144,41 @@ __device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT
   __syncthreads();
 }
 
+
+// ---- per-warp double-buffered staging of a contiguous observation segment ----
+constexpr int CH = 64;                         // observations per staged chunk
+constexpr int CH_BUF = CH * 32 + CH * 16 + (CH + 8) * 4;  // x, m, ids (one buffer)
+constexpr int CAM_WARP_SMEM = 2 * CH_BUF;      // two buffers per warp
+constexpr int CAM_SMEM = 8 * CAM_WARP_SMEM;    // 8 warps per CTA
+
+__device__ __forceinline__ void cp_async16w(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// stage observations [o, o + CH) of the camera-sorted streams (x, m and one int array)
+__device__ __forceinline__ void stage_chunk(unsigned char* buf, int lane, int o,
+                                            const double* __restrict__ cs_x,
+                                            const double* __restrict__ cs_m,
+                                            const int* __restrict__ ids) {
+  const char* gx = reinterpret_cast<const char*>(cs_x + 4 * (size_t)o);
+#pragma unroll
+  for (int q = 0; q < (CH * 32) / (16 * 32); ++q)
+    cp_async16w(buf + 16 * (lane + 32 * q), gx + 16 * (lane + 32 * q));
+  const char* gm = reinterpret_cast<const char*>(cs_m + 2 * (size_t)o);
+#pragma unroll
+  for (int q = 0; q < (CH * 16) / (16 * 32); ++q)
+    cp_async16w(buf + CH * 32 + 16 * (lane + 32 * q), gm + 16 * (lane + 32 * q));
+  const int a0 = o & ~3;
+  if (lane < (CH + 8) / 4)
+    cp_async16w(buf + CH * 48 + 16 * lane, ids + a0 + 4 * lane);
+}
+
 struct CamArgs {
   int c_lo, c_hi;   // landmark-block range of the W t half (HC)
   int first_c;      // 1: overwrite the camera accumulator y, 0: add
@@ -155,152 +190,209 @@ struct CamArgs {
 };
 
 template <int STAGE, bool HC, int EP, bool HA>
-__global__ void __launch_bounds__(FT, 2) k_cam(
+__global__ void __launch_bounds__(256) k_cam(
     Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
     const double* __restrict__ tarr, double* __restrict__ sbuf, double* __restrict__ cy,
     double* __restrict__ cyr, const double* __restrict__ cbp, const double* __restrict__ cUi,
     double* __restrict__ cx, double* __restrict__ crhs, const double* __restrict__ ch,
     double* __restrict__ nrm, PowerCtl* __restrict__ ctl, volatile PowerCtl* host_ctl,
     unsigned* __restrict__ ticket, Coef k, Tune tune, CamArgs ca) {
+  // one warp per camera; each (camera, block) segment is contiguous in memory
   constexpr bool RHS = EP == EP_RHS;
   constexpr int D = STAGE == 1 ? 12 : 11;
-  __shared__ double red[(FT / 32) * 12];
-  __shared__ double ysm[12];
-  __shared__ double vsm[12];
   __shared__ bool last;
-  const int cam = blockIdx.x;
+  extern __shared__ __align__(32) unsigned char cam_dsm[];
   if (ca.check_stop && ctl->stopped) return;  // grid-uniform
-  const int tid = threadIdx.x;
-  const int* cbo = g.cam_blk + (size_t)cam * (g.n_blk + 1);
-  const double* cp = crec + (size_t)cam * CREC;
-  const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2v = ldg4(cp + 8);
+  const int lane = threadIdx.x & 31;
+  const int cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  unsigned char* wsm = cam_dsm + (size_t)(threadIdx.x >> 5) * CAM_WARP_SMEM;
+  const bool valid = cam < g.n_p;
+  const int np = g.n_p;
   const uint64_t pf = pol_sel(tune.pol_stream), pt = pol_sel(tune.pol_t),
                  ps = pol_sel(tune.pol_s);
-
-  if (HC) {  // y_i (+)= sum_{j in blocks [c_lo, c_hi)} W_ij t_j
-    const int o_lo = __ldg(cbo + ca.c_lo), o_hi = __ldg(cbo + ca.c_hi);
+  double4 P0 = make_double4(0, 0, 0, 0), P1 = P0, P2v = P0;
+  if (valid) {
+    const double* cp = crec + (size_t)cam * CREC;
+    P0 = ldg4(cp);
+    P1 = ldg4(cp + 4);
+    P2v = ldg4(cp + 8);
+  }
+  double yr = 0.0;  // lane r < 12: component r of this camera's y
+  if (HC && valid) {  // y_i (+)= sum_{j in blocks [c_lo, c_hi)} W_ij t_j
     double acc[12];
 #pragma unroll
     for (int i = 0; i < 12; ++i) acc[i] = 0.0;
-#pragma unroll 4
-    for (int o = o_lo + tid; o < o_hi; o += FT) {
-      const int j = ldgip(g.cs_lm + o, pf);
-      const double4 X = ldg4p(cs_x + 4 * (size_t)o, pf);
-      const double2 m = ldg2p(g.cs_m + 2 * (size_t)o, pf);
-      const double4 T = ldg4p(tarr + 4 * (size_t)j, pt);
-      const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
-      double sg[3];
-      proj_map<STAGE>(pj, dot4(P0, T), dot4(P1, T), dot4(P2v, T), sg[0], sg[1], sg[2]);
+    for (int b = ca.c_lo; b < ca.c_hi; ++b) {
+      const int o_lo = __ldg(g.seg + (size_t)b * np + cam);
+      const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
+      const int nch = (o_hi - o_lo + CH - 1) / CH;
+      if (nch > 0) stage_chunk(wsm, lane, o_lo, cs_x, g.cs_m, g.cs_lm);
+      cp_commit();
+      for (int c = 0; c < nch; ++c) {
+        unsigned char* buf = wsm + (c & 1) * CH_BUF;
+        if (c + 1 < nch) stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (c + 1) * CH, cs_x,
+                                     g.cs_m, g.cs_lm);
+        cp_commit();
+        cp_wait<1>();
+        __syncwarp();
+        const int o0 = o_lo + c * CH;
+        const double4* sx = reinterpret_cast<const double4*>(buf);
+        const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
+        const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
+        double4 T[CH / 32];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        acc[4 * c + 0] = fma(sg[c], X.x, acc[4 * c + 0]);
-        acc[4 * c + 1] = fma(sg[c], X.y, acc[4 * c + 1]);
-        acc[4 * c + 2] = fma(sg[c], X.z, acc[4 * c + 2]);
-        acc[4 * c + 3] = fma(sg[c], X.w, acc[4 * c + 3]);
-      }
-    }
-    block_sum12(acc, red, ysm);
-    if (tid < 12) {  // fixed-order accumulation over blocks (deterministic)
-      const double y = ca.first_c ? ysm[tid] : cy[(size_t)cam * 12 + tid] + ysm[tid];
-      cy[(size_t)cam * 12 + tid] = y;
-      ysm[tid] = y;
-    }
-    __syncthreads();
-    if (ca.project_y) {  // schur apply: tangent projection (stage 2) -> cyr
-      if (tid < 32) {
-        double u = tid < 12 ? ysm[tid] : 0.0;
-        if (STAGE == 2) {
-          const double h = tid < 12 ? ch[(size_t)cam * 12 + tid] : 0.0;
-          const double hu = warp_sum(h * u);
-          const double pr = u - 2.0 * h * hu;
-          u = __shfl_sync(PV_FULL, pr, (tid + 1) & 31);
-          if (tid >= 11) u = 0.0;
+        for (int r = 0; r < CH / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
         }
-        if (tid < 12) cyr[(size_t)cam * 12 + tid] = u;
+#pragma unroll
+        for (int r = 0; r < CH / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (o0 + q < o_hi) {
+            const double4 X = sx[q];
+            const double2 m = sm[q];
+            const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
+            double sg[3];
+            proj_map<STAGE>(pj, dot4(P0, T[r]), dot4(P1, T[r]), dot4(P2v, T[r]), sg[0], sg[1],
+                            sg[2]);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+              acc[4 * cc + 0] = fma(sg[cc], X.x, acc[4 * cc + 0]);
+              acc[4 * cc + 1] = fma(sg[cc], X.y, acc[4 * cc + 1]);
+              acc[4 * cc + 2] = fma(sg[cc], X.z, acc[4 * cc + 2]);
+              acc[4 * cc + 3] = fma(sg[cc], X.w, acc[4 * cc + 3]);
+            }
+          }
+        }
+        __syncwarp();
       }
-      return;
+      cp_wait<0>();
     }
-  }
-
-  if (EP != EP_NONE) {
-    if (tid < 32) {  // warp 0: rows r < D of U^-1
-      const bool row = tid < 12;
-      double u = 0.0;
-      if (row) u = HC ? ysm[tid] : cy[(size_t)cam * 12 + tid];
-      double h = 0.0;
-      if (STAGE == 2) {  // project y (12) -> tangent (11)
-        h = row ? ch[(size_t)cam * 12 + tid] : 0.0;
+    warp_reduce_all(acc);
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+      if (lane == i) yr = acc[i];
+    if (lane < 12) {  // fixed-order accumulation over blocks (deterministic)
+      if (!ca.first_c) yr += cy[(size_t)cam * 12 + lane];
+      cy[(size_t)cam * 12 + lane] = yr;
+    }
+    if (ca.project_y) {  // schur apply: tangent projection (stage 2) -> cyr
+      double u = lane < 12 ? yr : 0.0;
+      if (STAGE == 2) {
+        const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
         const double hu = warp_sum(h * u);
         const double pr = u - 2.0 * h * hu;
-        u = __shfl_sync(PV_FULL, pr, (tid + 1) & 31);
-        if (tid >= 11) u = 0.0;
+        u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
+        if (lane >= 11) u = 0.0;
       }
-      double vin = u;
-      if (RHS) {
-        const double b = tid < D ? cbp[(size_t)cam * 12 + tid] : 0.0;
-        vin = tid < D ? -(b - u) : 0.0;
-        if (row) crhs[(size_t)cam * 12 + tid] = vin;
-      }
-      double t = 0.0;
-      const double* Ui = cUi + (size_t)cam * 144 + (tid < D ? tid : 0) * 12;
-#pragma unroll
-      for (int kk = 0; kk < 12; ++kk) {
-        const double vk = __shfl_sync(PV_FULL, vin, kk);
-        if (tid < D && kk < D) t = fma(Ui[kk], vk, t);
-      }
-      double xr = 0.0;
-      if (tid < D) {
-        xr = RHS ? t : cx[(size_t)cam * 12 + tid] + t;
-        cx[(size_t)cam * 12 + tid] = xr;
-      }
-      double v = t;
-      if (STAGE == 2) {  // v = B t (11 -> 12)
-        const double tprev = __shfl_sync(PV_FULL, t, (tid + 31) & 31);
-        const double e = (tid >= 1 && tid < 12) ? tprev : 0.0;
-        const double hd = warp_sum(h * e);
-        v = e - 2.0 * h * hd;
-      }
-      if (row) {
-        vsm[tid] = v;
-        crec[(size_t)cam * CREC + 12 + tid] = v;  // term vector for the later blocks
-      }
-      const double tn = warp_sum(tid < D ? t * t : 0.0);
-      const double xn = warp_sum(tid < D ? xr * xr : 0.0);
-      if (tid == 0) {
-        nrm[2 * (size_t)cam] = tn;
-        nrm[2 * (size_t)cam + 1] = xn;
-      }
+      if (lane < 12) cyr[(size_t)cam * 12 + lane] = u;
     }
-    __syncthreads();
-  } else if (HA) {
-    if (tid < 12) vsm[tid] = cp[12 + tid];
-    __syncthreads();
   }
 
-  if (HA) {  // s_ij = W_ij^T v_i for j in blocks [a_lo, a_hi), scattered (landmark order)
-    const double4 v0 = make_double4(vsm[0], vsm[1], vsm[2], vsm[3]);
-    const double4 v1 = make_double4(vsm[4], vsm[5], vsm[6], vsm[7]);
-    const double4 v2 = make_double4(vsm[8], vsm[9], vsm[10], vsm[11]);
-    const int o_lo = __ldg(cbo + ca.a_lo), o_hi = __ldg(cbo + ca.a_hi);
-#pragma unroll 4
-    for (int o = o_lo + tid; o < o_hi; o += FT) {
-      const int pos = ldgip(g.cs_pos + o, pf);
-      const double4 X = ldg4p(cs_x + 4 * (size_t)o, pf);
-      const double2 m = ldg2p(g.cs_m + 2 * (size_t)o, pf);
-      const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
-      double f0, f1, f2;
-      proj_map<STAGE>(pj, dot4(X, v0), dot4(X, v1), dot4(X, v2), f0, f1, f2);
-      double4 sv;
-      sv.x = fma(f0, P0.x, fma(f1, P1.x, f2 * P2v.x));
-      sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
-      sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
-      sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
-      st4p(sbuf + 4 * (size_t)pos, sv, ps);
+  double4 v0 = make_double4(0, 0, 0, 0), v1 = v0, v2 = v0;
+  if (EP != EP_NONE) {
+    const bool row = lane < 12;
+    double u = 0.0;
+    if (row && valid) u = HC ? yr : cy[(size_t)cam * 12 + lane];
+    double h = 0.0;
+    if (STAGE == 2) {  // project y (12) -> tangent (11)
+      h = (row && valid) ? ch[(size_t)cam * 12 + lane] : 0.0;
+      const double hu = warp_sum(h * u);
+      const double pr = u - 2.0 * h * hu;
+      u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
+      if (lane >= 11) u = 0.0;
+    }
+    double vin = u;
+    if (RHS) {
+      const double b = (lane < D && valid) ? cbp[(size_t)cam * 12 + lane] : 0.0;
+      vin = lane < D ? -(b - u) : 0.0;
+      if (row && valid) crhs[(size_t)cam * 12 + lane] = vin;
+    }
+    double t = 0.0;
+    const double* Ui = cUi + (size_t)(valid ? cam : 0) * 144 + (lane < D ? lane : 0) * 12;
+#pragma unroll
+    for (int kk = 0; kk < 12; ++kk) {
+      const double vk = __shfl_sync(PV_FULL, vin, kk);
+      if (valid && lane < D && kk < D) t = fma(Ui[kk], vk, t);
+    }
+    double xr = 0.0;
+    if (valid && lane < D) {
+      xr = RHS ? t : cx[(size_t)cam * 12 + lane] + t;
+      cx[(size_t)cam * 12 + lane] = xr;
+    }
+    double v = t;
+    if (STAGE == 2) {  // v = B t (11 -> 12)
+      const double tprev = __shfl_sync(PV_FULL, t, (lane + 31) & 31);
+      const double e = (lane >= 1 && lane < 12) ? tprev : 0.0;
+      const double hd = warp_sum(h * e);
+      v = e - 2.0 * h * hd;
+    }
+    if (row && valid) crec[(size_t)cam * CREC + 12 + lane] = v;  // for the later blocks
+    v0 = make_double4(__shfl_sync(PV_FULL, v, 0), __shfl_sync(PV_FULL, v, 1),
+                      __shfl_sync(PV_FULL, v, 2), __shfl_sync(PV_FULL, v, 3));
+    v1 = make_double4(__shfl_sync(PV_FULL, v, 4), __shfl_sync(PV_FULL, v, 5),
+                      __shfl_sync(PV_FULL, v, 6), __shfl_sync(PV_FULL, v, 7));
+    v2 = make_double4(__shfl_sync(PV_FULL, v, 8), __shfl_sync(PV_FULL, v, 9),
+                      __shfl_sync(PV_FULL, v, 10), __shfl_sync(PV_FULL, v, 11));
+    const double tn = warp_sum(lane < D ? t * t : 0.0);
+    const double xn = warp_sum(lane < D ? xr * xr : 0.0);
+    if (lane == 0 && valid) {
+      nrm[2 * (size_t)cam] = tn;
+      nrm[2 * (size_t)cam + 1] = xn;
+    }
+  } else if (HA && valid) {
+    const double* cp = crec + (size_t)cam * CREC + 12;
+    v0 = ldg4(cp);
+    v1 = ldg4(cp + 4);
+    v2 = ldg4(cp + 8);
+  }
+
+  if (HA && valid) {  // s_ij = W_ij^T v_i for j in blocks [a_lo, a_hi), scattered
+    for (int b = ca.a_lo; b < ca.a_hi; ++b) {
+      const int o_lo = __ldg(g.seg + (size_t)b * np + cam);
+      const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
+      const int nch = (o_hi - o_lo + CH - 1) / CH;
+      if (nch > 0) stage_chunk(wsm, lane, o_lo, cs_x, g.cs_m, g.cs_pos);
+      cp_commit();
+      for (int c = 0; c < nch; ++c) {
+        unsigned char* buf = wsm + (c & 1) * CH_BUF;
+        if (c + 1 < nch) stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (c + 1) * CH, cs_x,
+                                     g.cs_m, g.cs_pos);
+        cp_commit();
+        cp_wait<1>();
+        __syncwarp();
+        const int o0 = o_lo + c * CH;
+        const double4* sx = reinterpret_cast<const double4*>(buf);
+        const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
+        const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
+#pragma unroll
+        for (int r = 0; r < CH / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (o0 + q < o_hi) {
+            const double4 X = sx[q];
+            const double2 m = sm[q];
+            const int pos = si[q];
+            const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
+            double f0, f1, f2;
+            proj_map<STAGE>(pj, dot4(X, v0), dot4(X, v1), dot4(X, v2), f0, f1, f2);
+            double4 sv;
+            sv.x = fma(f0, P0.x, fma(f1, P1.x, f2 * P2v.x));
+            sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
+            sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
+            sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
+            st4p(sbuf + 4 * (size_t)pos, sv, ps);
+          }
+        }
+        __syncwarp();
+      }
+      cp_wait<0>();
     }
   }
 
   if (EP == EP_NONE) return;
   // ---- grid-wide fixed-order norm reduction + stop test in the last CTA
+  const int tid = threadIdx.x;
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
     const unsigned tk = atomicAdd(ticket, 1u);
@@ -310,13 +402,13 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
   if (!last) return;
   __threadfence();
   double a = 0.0, bsum = 0.0;
-  for (int i = tid; i < g.n_p; i += FT) {
+  for (int i = tid; i < g.n_p; i += blockDim.x) {
     a += __ldcg(nrm + 2 * (size_t)i);
     bsum += __ldcg(nrm + 2 * (size_t)i + 1);
   }
   double ra[2] = {a, bsum};
   warp_reduce_all(ra);
-  __shared__ double rr[2][FT / 32];
+  __shared__ double rr[2][8];
   if ((tid & 31) == 0) {
     rr[0][tid >> 5] = ra[0];
     rr[1][tid >> 5] = ra[1];
@@ -324,7 +416,7 @@ __global__ void __launch_bounds__(FT, 2) k_cam(
   __syncthreads();
   if (tid == 0) {
     double TN2 = 0.0, XN2 = 0.0;
-    for (int q = 0; q < FT / 32; ++q) {
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
       TN2 += rr[0][q];
       XN2 += rr[1][q];
     }
@@ -438,10 +530,10 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
   }
 }
 
-constexpr int LR_BATCH = 4;  // landmark tasks per warp (loads of all of them in flight)
+constexpr int LR_BATCH = 2;  // landmark tasks per warp (loads of all of them in flight)
 
 template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__ sbuf,
+__global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restrict__ sbuf,
                                                    const double* __restrict__ lrec,
                                                    double* __restrict__ tarr,
                                                    const double* __restrict__ lsys,
@@ -514,6 +606,14 @@ __global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__
     for (size_t ln = l0 + lane; ln < l1; ln += 32)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + ln * 128) : "memory");
   }
+}
+
+// block-major camera-sorted copy of the measurements (once per re-blocking)
+__global__ void k_gather_m(int n_o, const int* __restrict__ cs_pos, const double* __restrict__ ls_m,
+                           double* __restrict__ cs_m) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n_o) return;
+  reinterpret_cast<double2*>(cs_m)[o] = reinterpret_cast<const double2*>(ls_m)[__ldg(cs_pos + o)];
 }
 
 // camera-sorted copy of the landmark coordinates (once per linearization point)
@@ -668,13 +768,14 @@ __global__ void __launch_bounds__(FT) k_lin_cam(Graph g, const double* __restric
   __shared__ double red[(FT / 32) * NA];
   __shared__ double tot[NA];
   const int cam = blockIdx.x, tid = threadIdx.x;
-  const int o0 = g.cam_off[cam], o1 = g.cam_off[cam + 1];
   const double* cp = crec + (size_t)cam * CREC;
   const double4 P0 = ldg4(cp), P1 = ldg4(cp + 4), P2 = ldg4(cp + 8);
   double acc[NA];
 #pragma unroll
   for (int i = 0; i < NA; ++i) acc[i] = 0.0;
-  for (int o = o0 + tid; o < o1; o += FT) {
+  for (int b = 0; b < g.n_blk; ++b)
+  for (int o = g.seg[(size_t)b * g.n_p + cam] + tid; o < g.seg[(size_t)b * g.n_p + cam + 1];
+       o += FT) {
     const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
     const double4 X = ldg4(cs_x + 4 * (size_t)o);
     const double u0 = dot4(P0, X), u1 = dot4(P1, X), u2 = dot4(P2, X);

@@ -28,6 +28,9 @@ pols = [tuple(int(x) for x in p) for p in os.environ.get("POLS", "122,000").spli
 discs = [int(x) for x in os.environ.get("DISC", "1,0").split(",")]
 for mb, (ps, pt, pss), disc in itertools.product(blocks, pols, discs):
     dp.set_option(_lib.PV_OPT_BLOCK_BYTES, mb << 20)
+    dp.linearize(stage)  # re-blocking reorders the camera-sorted arrays
+    dp.damp(1e-4, stage == 2)
+    dp.power_solve(1, 0.0)
     dp.set_option(_lib.PV_OPT_POL_STREAM, ps)
     dp.set_option(_lib.PV_OPT_POL_T, pt)
     dp.set_option(_lib.PV_OPT_POL_S, pss)
