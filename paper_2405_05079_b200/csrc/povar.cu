@@ -75,6 +75,7 @@ struct pv_ctx {
   int64_t block_bytes = 80ll << 20;
   size_t seg_bytes = 0;
   int64_t persist_l2 = 0;
+  bool lm_lin_fresh = false;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
@@ -115,6 +116,13 @@ struct pv_ctx {
   void sync() { CK(cudaStreamSynchronize(stream)); }
 
   int nblk_tasks() const { return blocks_for((long long)n_tasks * 32, 256); }
+  // deterministic sum of n_tasks warp partials into scal[0] (two levels)
+  void sum_partials() {
+    const int nb2 = std::max(1, std::min(256, (n_tasks + 4095) / 4096));
+    k_sum<<<nb2, 1024, 0, stream>>>(cpart, std::max(n_tasks, 1), cpart + n_tasks + 8);
+    k_sum<<<1, 1024, 0, stream>>>(cpart + n_tasks + 8, nb2, scal);
+    launched(2);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -340,7 +348,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->cyr = c->alloc<double>(np * 12);
   c->cUraw = c->alloc<double>(np * LINP);
   c->nrm = c->alloc<double>(np * 2);
-  c->cpart = c->alloc<double>((size_t)c->nblk_tasks());
+  c->cpart = c->alloc<double>((size_t)c->n_tasks + 8 + 256);  // warp partials + level 2
   c->ctmp = c->alloc<double>(np * 12);
   c->scal = c->alloc<double>(8);
   c->flags = c->alloc<int>(F_COUNT);
@@ -361,10 +369,10 @@ static void op_cost(pv_ctx* c, int which, double* f) {
   const double* lms = which == PV_TRIAL ? c->tlm : c->lrec;
   const int ls = which == PV_TRIAL ? 4 : LREC;
   CK(cudaMemsetAsync(c->flags + F_INVALID_Z, 0, sizeof(int), c->stream));
-  const int nb = c->nblk_tasks();
-  k_cost<S><<<nb, 256, 0, c->stream>>>(c->g, cams, cs, lms, ls, c->cpart, c->flags, c->coef);
-  k_sum<<<1, 1024, 0, c->stream>>>(c->cpart, nb, c->scal);
-  c->launched(2);
+  k_cost<S><<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
+      c->g, cams, cs, lms, ls, c->cpart, c->flags, c->coef);
+  c->launched();
+  c->sum_partials();
   c->check_launch();
   c->allreduce(c->scal, 1);
   c->allreduce_flags();
@@ -380,10 +388,14 @@ template <int S>
 static int op_linearize(pv_ctx* c) {
   CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
   k_build_csx<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x);
-  k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr, c->lbl,
-                                                      c->flags, c->coef);
+  if (!(S == 1 && c->lm_lin_fresh)) {
+    k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr, c->lbl,
+                                                        c->flags, c->coef);
+    c->launched();
+  }
+  c->lm_lin_fresh = false;
   k_lin_cam<S><<<(int)c->n_p, FT, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->cUraw, c->coef);
-  c->launched(3);
+  c->launched(2);
   c->check_launch();
   c->allreduce(c->cUraw, (size_t)c->n_p * LINP);
   k_lin_cam_project<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>(
@@ -539,10 +551,10 @@ static void op_trial(pv_ctx* c, int* ok) {
 
 static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
   CK(cudaMemsetAsync(c->flags + F_N_RANKDEF, 0, 2 * sizeof(int), c->stream));
-  const int nb = c->nblk_tasks();
-  k_resolve<<<nb, 256, 0, c->stream>>>(c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef);
-  k_sum<<<1, 1024, 0, c->stream>>>(c->cpart, nb, c->scal);
-  c->launched(2);
+  k_resolve<<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
+      c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef, c->lvr, c->lbl);
+  c->launched();
+  c->sum_partials();
   c->check_launch();
   c->allreduce(c->scal, 1);
   c->allreduce_flags();
@@ -556,7 +568,7 @@ static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
   c->last_fallbacks = fl[F_N_FALLBACK];
 }
 
-static void op_accept(pv_ctx* c) {
+static void op_accept(pv_ctx* c, bool lm_lin_fresh = false) {
   const int n = (int)std::max<int64_t>(c->n_p, c->n_ls);
   k_accept<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)c->n_p, c->n_ls, c->tcam, c->tlm,
                                                       c->crec, c->lrec);
@@ -564,6 +576,7 @@ static void op_accept(pv_ctx* c) {
   c->check_launch();
   c->lin_stage = 0;
   c->vp_cached = false;
+  c->lm_lin_fresh = lm_lin_fresh;  // the re-solve already produced V, b_l at this state
 }
 
 // ---------------------------------------------------------------------------
@@ -758,6 +771,7 @@ int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
   c->sync();
   c->lin_stage = 0;
   c->vp_cached = false;
+  c->lm_lin_fresh = false;
   API_END(c)
 }
 
@@ -852,7 +866,7 @@ int pv_accept(pv_ctx* c, int stage, int resolve, double* f_new, int64_t* n_rd) {
     if (stage != 1) throw PvError(PV_EINVAL, "landmark re-solve is a stage-1 operation");
     op_resolve_trial(c, f_new, n_rd);
   }
-  op_accept(c);
+  op_accept(c, resolve != 0);
   c->sync();
   API_END(c)
 }
@@ -865,7 +879,7 @@ int pv_resolve_current(pv_ctx* c, int64_t* n_rd) {
                                                          c->tcam, c->tlm);
   c->launched();
   op_resolve_trial(c, nullptr, n_rd);
-  op_accept(c);
+  op_accept(c, true);
   c->sync();
   API_END(c)
 }
