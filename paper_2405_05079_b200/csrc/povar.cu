@@ -508,9 +508,11 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
   c->sync();
   std::memset(c->host_ctl, 0, sizeof(PowerCtl));
-  // K4: t = V+ b_l, reduced RHS over all blocks, t_0 = U^-1 rhs, gather of block 0
+  // K4: t = V+ b_l for all landmarks, then y = W t over all blocks, the reduced RHS,
+  // t_0 = U^-1 rhs and the gather of block 0 (a single pass; blocking does not pay here)
+  const int B = c->n_blk;
   launch_lm_reduce<S, LR_RHS>(c, 0, c->n_tasks, 0);
-  launch_cam_last<S, EP_RHS>(c, 0, c->n_blk, 1, 0, thr, 0);
+  launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, thr, 0);
   c->check_launch();
   // K5 + K6 terms with a one-term lookahead on the device stop flag
   for (int i = 1; i <= max_order; ++i) {
@@ -522,11 +524,13 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     }
   }
   c->check_launch();
-  // K7 back-substitution with v = x (all blocks at once)
+  // K7 back-substitution with v = x, block by block (s stays in L2)
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
   c->launched();
-  launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, c->n_blk, 0, thr, 0));
-  launch_lm_reduce<S, LR_BACKSUB>(c, 0, c->n_tasks, 0);
+  for (int b = 0; b < B; ++b) {
+    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, b, b + 1, 0, thr, 0));
+    launch_lm_reduce<S, LR_BACKSUB>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+  }
   c->check_launch();
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));

@@ -712,7 +712,8 @@ __device__ __forceinline__ void lin_lm_finish(int l, const double (&acc)[14], co
     basis_apply_t<4>(h, bb, b3);
   }
   double* o = lvr + (size_t)l * 8;
-  for (int i = 0; i < 6; ++i) o[i] = V6[i];
+  st4(o, make_double4(V6[0], V6[1], V6[2], V6[3]));
+  st4(o + 4, make_double4(V6[4], V6[5], 0.0, 0.0));
   st4(lbl + (size_t)l * 4, make_double4(b3[0], b3[1], b3[2], 0.0));
 }
 
@@ -1032,7 +1033,32 @@ __global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const double*
       V6[5] = damp_diag(V6[5], lam);
     }
     double P6[6];
-    degen = pinv_sym3(V6, 1e-10, P6);
+    // Fast path: Cholesky.  lambda_min >= det / lambda_max^2 >= det / trace^2, so
+    // det > 1e-9 trace^3 certifies that no eigenvalue falls under the reference cutoff
+    // (1e-10 trace, normal_eq.py:145-153): the pseudo-inverse is the inverse.
+    const double tr = V6[0] + V6[3] + V6[5];
+    const double d0 = V6[0];
+    const double r00 = d0 > 0.0 ? sqrt(d0) : 1.0;
+    const double r01 = V6[1] / r00, r02 = V6[2] / r00;
+    const double d1 = V6[3] - r01 * r01;
+    const double r11 = d1 > 0.0 ? sqrt(d1) : 1.0;
+    const double r12 = (V6[4] - r01 * r02) / r11;
+    const double d2 = V6[5] - r02 * r02 - r12 * r12;
+    if (d0 > 0.0 && d1 > 0.0 && d2 > 0.0 && d0 * d1 * d2 > 1e-9 * tr * tr * tr) {
+      const double r22 = sqrt(d2);
+      const double i00 = 1.0 / r00, i11 = 1.0 / r11, i22 = 1.0 / r22;
+      const double i01 = -r01 * i00 * i11, i12 = -r12 * i11 * i22;
+      const double i02 = -(r01 * i12 + r02 * i22) * i00;
+      P6[0] = i00 * i00 + i01 * i01 + i02 * i02;
+      P6[1] = i01 * i11 + i02 * i12;
+      P6[2] = i02 * i22;
+      P6[3] = i11 * i11 + i12 * i12;
+      P6[4] = i12 * i22;
+      P6[5] = i22 * i22;
+      degen = false;
+    } else {
+      degen = pinv_sym3(V6, 1e-10, P6);
+    }
     double* o = lsys + (size_t)l * LSYS;
     st4(o, make_double4(P6[0], P6[1], P6[2], P6[3]));
     st4(o + 4, make_double4(P6[4], P6[5], degen ? 1.0 : 0.0, 0.0));
@@ -1342,7 +1368,7 @@ __device__ __forceinline__ double rows_cost(const Rows4& rw, const double4& x) {
   return f;
 }
 
-__global__ void __launch_bounds__(64) k_resolve(Graph g, const double* __restrict__ tcam,
+__global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __restrict__ tcam,
                                                  double* __restrict__ tlm,
                                                  double* __restrict__ part, int* flags, Coef k,
                                                  double* __restrict__ lvr, double* __restrict__ lbl) {
@@ -1443,7 +1469,8 @@ __global__ void __launch_bounds__(64) k_resolve(Graph g, const double* __restric
         // the next stage-1 linearization at this state: V = A^T A (J_l does not depend
         // on x) and b_l = J_l^T r = A^T (A x + c)
         double* vo = lvr + (size_t)l * 8;
-        for (int i = 0; i < 6; ++i) vo[i] = g1[i];
+        st4(vo, make_double4(g1[0], g1[1], g1[2], g1[3]));
+        st4(vo + 4, make_double4(g1[4], g1[5], 0.0, 0.0));
         const double b0 = fma(g1[0], xn[0], fma(g1[1], xn[1], fma(g1[2], xn[2], g1[6] * xn[3])));
         const double b1 = fma(g1[1], xn[0], fma(g1[3], xn[1], fma(g1[4], xn[2], g1[7] * xn[3])));
         const double b2 = fma(g1[2], xn[0], fma(g1[4], xn[1], fma(g1[5], xn[2], g1[8] * xn[3])));
