@@ -22,7 +22,7 @@ INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "
                "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2")
 PV_INFO_COUNT = 16
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
- PV_OPT_BLOCK_BYTES) = range(6)
+ PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE) = range(7)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
 _P = ctypes.c_void_p

@@ -107,11 +107,14 @@ struct pv_ctx {
   void launched(int n = 1) { launches += n; }
   void check_launch() { CK(cudaGetLastError()); }
 
+  // the collective (sharded) code path: world > 1, or forced on one GPU with a
+  // 1-rank NCCL communicator to exercise the split kernels + NCCL calls
+  bool collective() const { return comm != nullptr; }
   void allreduce(double* p, size_t n) {
-    if (world > 1) NK(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, stream));
+    if (comm) NK(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, stream));
   }
   void allreduce_flags() {
-    if (world > 1) NK(ncclAllReduce(flags, flags, F_COUNT, ncclInt32, ncclMax, comm, stream));
+    if (comm) NK(ncclAllReduce(flags, flags, F_COUNT, ncclInt32, ncclMax, comm, stream));
   }
   void sync() { CK(cudaStreamSynchronize(stream)); }
 
@@ -479,7 +482,7 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
 template <int S, int EP>
 static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term, double thr,
                             int check_stop) {
-  if (c->world == 1) {
+  if (!c->collective()) {
     launch_cam<S, true, EP, true>(c, cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop));
   } else {
     launch_cam<S, true, EP_NONE, false>(c,
@@ -738,8 +741,20 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_DISCARD_S:
       c->tune.discard_s = (int)value;
       break;
+    case PV_OPT_FORCE_COLLECTIVE:
+      if (value && !c->comm) {  // 1-rank communicator: same kernels/collectives as world > 1
+        if (c->world != 1) throw PvError(PV_EINVAL, "already collective");
+        ncclUniqueId id;
+        NK(ncclGetUniqueId(&id));
+        CK(cudaSetDevice(c->device));
+        NK(ncclCommInitRank(&c->comm, 1, id, 0));
+      } else if (!value && c->comm && c->world == 1) {
+        ncclCommDestroy(c->comm);
+        c->comm = nullptr;
+      }
+      break;
     case PV_OPT_BLOCK_BYTES:
-      if (value < (1 << 20)) throw PvError(PV_EINVAL, "block budget too small");
+      if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
       c->block_bytes = value;
       build_blocks(c);
       break;
@@ -919,30 +934,14 @@ static void op_schur_apply(pv_ctx* c, const double* v, double* out) {
   c->launched();
   launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, c->n_blk, 0, 0.0, 0));
   launch_lm_reduce<S, LR_TERM>(c, 0, c->n_tasks, 0);
-  CamArgs ca = cam_args(0, c->n_blk, 1, 0, 0, 0, 0.0, 0);
-  if (c->world == 1) ca.project_y = 1;
-  launch_cam<S, true, EP_NONE, false>(c, ca);
-  if (c->world > 1) {
-    c->allreduce(c->cy, (size_t)c->n_p * 12);
-    CK(cudaMemcpyAsync(c->cyr, c->cy, (size_t)c->n_p * 12 * 8, cudaMemcpyDeviceToDevice,
-                       c->stream));
-    if (S == 2) {  // project on the host copy below
-    }
-  }
+  launch_cam<S, true, EP_NONE, false>(c, cam_args(0, c->n_blk, 1, 0, 0, 0, 0.0, 0));
+  c->allreduce(c->cy, (size_t)c->n_p * 12);
+  k_project_y<S><<<blocks_for(c->n_p * 32, 256), 256, 0, c->stream>>>((int)c->n_p, c->cy, c->ch,
+                                                                     c->cyr);
+  c->launched();
   c->check_launch();
   CK(cudaMemcpyAsync(h.data(), c->cyr, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
-  if (c->world > 1 && S == 2) {  // tangent projection of the summed raw y
-    std::vector<double> hh((size_t)c->n_p * 12);
-    CK(cudaMemcpy(hh.data(), c->ch, hh.size() * 8, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < c->n_p; ++i) {
-      double hu = 0.0;
-      for (int q = 0; q < 12; ++q) hu += hh[i * 12 + q] * h[i * 12 + q];
-      double pr[12];
-      for (int q = 0; q < 12; ++q) pr[q] = h[i * 12 + q] - 2.0 * hh[i * 12 + q] * hu;
-      for (int q = 0; q < 11; ++q) h[i * 12 + q] = pr[q + 1];
-    }
-  }
   for (int64_t i = 0; i < c->n_p; ++i)
     for (int q = 0; q < D; ++q) out[i * D + q] = h[i * 12 + q];
 }

@@ -452,6 +452,24 @@ __global__ void __launch_bounds__(256) k_cam(
   }
 }
 
+// y (raw 12 per camera) -> tangent y (11) in stage 2 / copy in stage 1 (schur apply)
+template <int STAGE>
+__global__ void k_project_y(int n_p, const double* __restrict__ cy, const double* __restrict__ ch,
+                            double* __restrict__ cyr) {
+  const int lane = threadIdx.x & 31;
+  const int cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (cam >= n_p) return;
+  double u = lane < 12 ? cy[(size_t)cam * 12 + lane] : 0.0;
+  if (STAGE == 2) {
+    const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
+    const double hu = warp_sum(h * u);
+    const double pr = u - 2.0 * h * hu;
+    u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
+    if (lane >= 11) u = 0.0;
+  }
+  if (lane < 12) cyr[(size_t)cam * 12 + lane] = u;
+}
+
 // ---------------------------------------------------------------------------
 // landmark half of a term (and K7): t_j = V_j^+ sum_i s_ij (TERM) or V_j^+ b_j
 // (RHS) written per landmark, or the back-substitution
