@@ -548,19 +548,19 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
   }
 }
 
-constexpr int LR_BATCH = 2;  // landmark tasks per warp (loads of all of them in flight)
+constexpr int LR_BATCH = 2;  // landmark tasks per warp, all of their loads issued up front
 
 template <int STAGE, int MODE>
 __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restrict__ sbuf,
-                                                   const double* __restrict__ lrec,
-                                                   double* __restrict__ tarr,
-                                                   const double* __restrict__ lsys,
-                                                   const double* __restrict__ lbl,
-                                                   double* __restrict__ ldl,
-                                                   double* __restrict__ tlm,
-                                                   const PowerCtl* __restrict__ ctl, int* flags,
-                                                   Tune tune, int task_lo, int task_hi,
-                                                   int check_stop) {
+                                                      const double* __restrict__ lrec,
+                                                      double* __restrict__ tarr,
+                                                      const double* __restrict__ lsys,
+                                                      const double* __restrict__ lbl,
+                                                      double* __restrict__ ldl,
+                                                      double* __restrict__ tlm,
+                                                      const PowerCtl* __restrict__ ctl, int* flags,
+                                                      Tune tune, int task_lo, int task_hi,
+                                                      int check_stop) {
   const int lane = threadIdx.x & 31;
   const int w0 = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LR_BATCH;
   if (w0 >= task_hi) return;
@@ -571,7 +571,11 @@ __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restric
   if (lane < nb) d = __ldg(g.task + w0 + lane);
   Task tk[LR_BATCH];
   double4 sv[LR_BATCH];
+  LmPre pre[LR_BATCH];
+  int lm[LR_BATCH], send[LR_BATCH];
+  bool hd[LR_BATCH];
   int o_first = 0, o_end = 0;
+  // (1) every load of the batch in flight at once: partials s and the heads' V+
 #pragma unroll
   for (int q = 0; q < LR_BATCH; ++q) {
     tk[q].o0 = __shfl_sync(PV_FULL, d.x, q);
@@ -582,16 +586,26 @@ __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restric
     if (q == 0) o_first = tk[q].o0;
     if (q < nb) o_end = tk[q].o0 + tk[q].n;
     sv[q] = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (MODE != LR_RHS && q < nb && !tk[q].long_task && lane < tk[q].n)
-      sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
+    hd[q] = false;
+    lm[q] = tk[q].l0;
+    send[q] = 0;
+    if (q < nb && !tk[q].long_task) {
+      lane_segment(tk[q], lane, lm[q], send[q]);
+      hd[q] = lane < tk[q].n && ((tk[q].heads >> lane) & 1u);
+      if (MODE != LR_RHS && lane < tk[q].n)
+        sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
+    } else if (q < nb) {
+      hd[q] = lane == 0;
+    }
+    if (hd[q]) pre[q] = lm_prefetch<STAGE, MODE>(lm[q], lrec, lsys, lbl);
   }
+  // (2) reduce and finish
 #pragma unroll
   for (int q = 0; q < LR_BATCH; ++q) {
     if (q >= nb) break;
     const Task& t = tk[q];
+    double acc[4] = {sv[q].x, sv[q].y, sv[q].z, sv[q].w};
     if (t.long_task) {
-      const LmPre pre = lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl);
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
       if (MODE != LR_RHS) {
         for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
           const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
@@ -602,17 +616,10 @@ __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restric
         }
         warp_reduce_all(acc);
       }
-      if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
-    } else {
-      int l, seg_end;
-      lane_segment(t, lane, l, seg_end);
-      const bool head = lane < t.n && ((t.heads >> lane) & 1u);
-      LmPre pre;
-      if (head) pre = lm_prefetch<STAGE, MODE>(l, lrec, lsys, lbl);
-      double acc[4] = {sv[q].x, sv[q].y, sv[q].z, sv[q].w};
-      if (MODE != LR_RHS) seg_reduce(acc, lane, seg_end);
-      if (head) lm_finish<STAGE, MODE>(l, acc, pre, tarr, ldl, tlm, flags, pt);
+    } else if (MODE != LR_RHS) {
+      seg_reduce(acc, lane, send[q]);
     }
+    if (hd[q]) lm_finish<STAGE, MODE>(lm[q], acc, pre[q], tarr, ldl, tlm, flags, pt);
   }
   if (MODE == LR_TERM && tune.discard_s) {
     // the consumed partials are scratch: drop their L2 lines instead of writing them back
