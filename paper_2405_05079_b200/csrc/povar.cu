@@ -75,7 +75,9 @@ struct pv_ctx {
   int64_t block_bytes = 80ll << 20;
   size_t seg_bytes = 0;
   int64_t persist_l2 = 0;
-  bool lm_lin_fresh = false;  // lvr/lbl hold the stage-1 landmark linearization of the current state
+  bool lm_lin_fresh = false;
+  int num_sms = 148;
+  int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
@@ -455,11 +457,13 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca) {
 
 template <int S, int MODE>
 static void launch_lm_reduce(pv_ctx* c, int t_lo, int t_hi, int check_stop) {
-  const int nw = (t_hi - t_lo + LR_BATCH - 1) / LR_BATCH;
-  const int nb = blocks_for((long long)nw * 32, 256);
-  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
-                                                  c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
-                                                  c->tune, t_lo, t_hi, check_stop);
+  // persistent pipelined warps: about three resident CTAs of 8 warps per SM
+  const int nt = t_hi - t_lo;
+  const int want = std::max(1, std::min(blocks_for((long long)nt * 32, 256),
+                                        c->num_sms * c->lr_ctas_per_sm));
+  k_lm_reduce<S, MODE><<<want, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
+                                                    c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
+                                                    c->tune, t_lo, t_hi, check_stop);
   c->launched();
 }
 
@@ -663,6 +667,7 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
       c->persist_l2 = max_persist;
     }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     for (auto& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->tev) CK(cudaEventCreate(&e));
     if (world > 1) {

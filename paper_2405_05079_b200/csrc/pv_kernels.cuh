@@ -548,8 +548,81 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
   }
 }
 
-constexpr int LR_BATCH = 2;  // landmark tasks per warp, all of their loads issued up front
+constexpr int LR_BATCH = 2;  // (non-pipelined launches) tasks per warp
 
+// per-task registers of the pipelined landmark reduce
+struct LrSlot {
+  Task t;
+  double4 sv;
+  LmPre pre;
+  int lm, send;
+  bool hd, valid;
+};
+
+template <int STAGE, int MODE>
+__device__ __forceinline__ void lr_issue(const Graph& g, const double* __restrict__ sbuf,
+                                         const double* __restrict__ lrec,
+                                         const double* __restrict__ lsys,
+                                         const double* __restrict__ lbl, int4 d, bool valid,
+                                         int lane, uint64_t pf, LrSlot& sl) {
+  sl.valid = valid;
+  sl.t.o0 = d.x;
+  sl.t.n = d.y;
+  sl.t.l0 = d.z;
+  sl.t.heads = (unsigned)d.w;
+  sl.t.long_task = sl.t.n > 32;
+  sl.sv = make_double4(0.0, 0.0, 0.0, 0.0);
+  sl.hd = false;
+  sl.lm = sl.t.l0;
+  sl.send = 0;
+  if (!valid) return;
+  if (!sl.t.long_task) {
+    lane_segment(sl.t, lane, sl.lm, sl.send);
+    sl.hd = lane < sl.t.n && ((sl.t.heads >> lane) & 1u);
+    if (MODE != LR_RHS && lane < sl.t.n) sl.sv = ldg4p(sbuf + 4 * (size_t)(sl.t.o0 + lane), pf);
+  } else {
+    sl.hd = lane == 0;
+  }
+  if (sl.hd) sl.pre = lm_prefetch<STAGE, MODE>(sl.lm, lrec, lsys, lbl);
+}
+
+template <int STAGE, int MODE>
+__device__ __forceinline__ void lr_finish(const LrSlot& sl, int lane, double* __restrict__ sbuf,
+                                          double* __restrict__ tarr, double* __restrict__ ldl,
+                                          double* __restrict__ tlm, int* __restrict__ flags,
+                                          uint64_t pf, uint64_t pt, int discard) {
+  if (!sl.valid) return;
+  const Task& t = sl.t;
+  double acc[4] = {sl.sv.x, sl.sv.y, sl.sv.z, sl.sv.w};
+  if (t.long_task) {
+    if (MODE != LR_RHS) {
+      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
+        const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
+        acc[0] += s.x;
+        acc[1] += s.y;
+        acc[2] += s.z;
+        acc[3] += s.w;
+      }
+      warp_reduce_all(acc);
+    }
+  } else if (MODE != LR_RHS) {
+    seg_reduce(acc, lane, sl.send);
+  }
+  if (sl.hd) lm_finish<STAGE, MODE>(sl.lm, acc, sl.pre, tarr, ldl, tlm, flags, pt);
+  if (MODE == LR_TERM && discard) {
+    // consumed partials are scratch: drop their L2 lines (only lines inside this task)
+    const size_t b0 = 4 * (size_t)t.o0 * sizeof(double);
+    const size_t b1 = 4 * (size_t)(t.o0 + t.n) * sizeof(double);
+    const size_t l0 = (b0 + 127) / 128, l1 = b1 / 128;
+    char* base = reinterpret_cast<char*>(sbuf);
+    for (size_t ln = l0 + lane; ln < l1; ln += 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + ln * 128) : "memory");
+  }
+}
+
+// Persistent, software-pipelined landmark reduce: each warp walks tasks
+// w, w + NW, w + 2 NW, ...; while task i reduces, the loads of task i + NW (s and
+// the heads' V+) and the descriptor of task i + 2 NW are already in flight.
 template <int STAGE, int MODE>
 __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restrict__ sbuf,
                                                       const double* __restrict__ lrec,
@@ -562,74 +635,26 @@ __global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restric
                                                       Tune tune, int task_lo, int task_hi,
                                                       int check_stop) {
   const int lane = threadIdx.x & 31;
-  const int w0 = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LR_BATCH;
-  if (w0 >= task_hi) return;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  int ti = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (ti >= task_hi) return;
   if (check_stop && ctl->stopped) return;
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
-  const int nb = min(LR_BATCH, task_hi - w0);
-  int4 d = make_int4(0, 0, 0, 0);
-  if (lane < nb) d = __ldg(g.task + w0 + lane);
-  Task tk[LR_BATCH];
-  double4 sv[LR_BATCH];
-  LmPre pre[LR_BATCH];
-  int lm[LR_BATCH], send[LR_BATCH];
-  bool hd[LR_BATCH];
-  int o_first = 0, o_end = 0;
-  // (1) every load of the batch in flight at once: partials s and the heads' V+
-#pragma unroll
-  for (int q = 0; q < LR_BATCH; ++q) {
-    tk[q].o0 = __shfl_sync(PV_FULL, d.x, q);
-    tk[q].n = __shfl_sync(PV_FULL, d.y, q);
-    tk[q].l0 = __shfl_sync(PV_FULL, d.z, q);
-    tk[q].heads = (unsigned)__shfl_sync(PV_FULL, d.w, q);
-    tk[q].long_task = tk[q].n > 32;
-    if (q == 0) o_first = tk[q].o0;
-    if (q < nb) o_end = tk[q].o0 + tk[q].n;
-    sv[q] = make_double4(0.0, 0.0, 0.0, 0.0);
-    hd[q] = false;
-    lm[q] = tk[q].l0;
-    send[q] = 0;
-    if (q < nb && !tk[q].long_task) {
-      lane_segment(tk[q], lane, lm[q], send[q]);
-      hd[q] = lane < tk[q].n && ((tk[q].heads >> lane) & 1u);
-      if (MODE != LR_RHS && lane < tk[q].n)
-        sv[q] = ldg4p(sbuf + 4 * (size_t)(tk[q].o0 + lane), pf);
-    } else if (q < nb) {
-      hd[q] = lane == 0;
-    }
-    if (hd[q]) pre[q] = lm_prefetch<STAGE, MODE>(lm[q], lrec, lsys, lbl);
-  }
-  // (2) reduce and finish
-#pragma unroll
-  for (int q = 0; q < LR_BATCH; ++q) {
-    if (q >= nb) break;
-    const Task& t = tk[q];
-    double acc[4] = {sv[q].x, sv[q].y, sv[q].z, sv[q].w};
-    if (t.long_task) {
-      if (MODE != LR_RHS) {
-        for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-          const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
-          acc[0] += s.x;
-          acc[1] += s.y;
-          acc[2] += s.z;
-          acc[3] += s.w;
-        }
-        warp_reduce_all(acc);
-      }
-    } else if (MODE != LR_RHS) {
-      seg_reduce(acc, lane, send[q]);
-    }
-    if (hd[q]) lm_finish<STAGE, MODE>(lm[q], acc, pre[q], tarr, ldl, tlm, flags, pt);
-  }
-  if (MODE == LR_TERM && tune.discard_s) {
-    // the consumed partials are scratch: drop their L2 lines instead of writing them back
-    // (only lines entirely inside this warp's observation range)
-    const size_t b0 = 4 * (size_t)o_first * sizeof(double);
-    const size_t b1 = 4 * (size_t)o_end * sizeof(double);
-    const size_t l0 = (b0 + 127) / 128, l1 = b1 / 128;
-    char* base = reinterpret_cast<char*>(sbuf);
-    for (size_t ln = l0 + lane; ln < l1; ln += 32)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + ln * 128) : "memory");
+  auto desc = [&](int i) {
+    return i < task_hi ? __ldg(g.task + i) : make_int4(0, 0, 0, 0);
+  };
+  LrSlot cur;
+  lr_issue<STAGE, MODE>(g, sbuf, lrec, lsys, lbl, desc(ti), true, lane, pf, cur);
+  int4 dn = desc(ti + nw);
+  while (true) {
+    const int tn = ti + nw;
+    LrSlot nxt;
+    lr_issue<STAGE, MODE>(g, sbuf, lrec, lsys, lbl, dn, tn < task_hi, lane, pf, nxt);
+    dn = desc(tn + nw);
+    lr_finish<STAGE, MODE>(cur, lane, sbuf, tarr, ldl, tlm, flags, pf, pt, tune.discard_s);
+    if (tn >= task_hi) break;
+    cur = nxt;
+    ti = tn;
   }
 }
 
