@@ -25,12 +25,11 @@ constexpr int LREC = 4;   // landmark record: x (4)
 constexpr int LSYS = 8;   // V+ (6) | degenerate (1) | pad
 constexpr int LINP = 90;  // camera linearization: U upper (78) | b_p (12)
 constexpr int FT = 256;   // threads of a camera CTA
-constexpr int CM_STAGE_MAX = 2048;  // max observations of a camera staged in shared memory
 
 // runtime tuning of the term kernels (pv_set_option): on-chip staging capacity
 // and L2 eviction priorities (0 normal, 1 evict_first, 2 evict_last)
 struct Tune {
-  int stage_cap;   // (unused by the blocked term)
+  int stage_cap;   // reserved (ABI stability of pv_set_option)
   int pol_stream;  // camera-sorted streams (m, x, ids)
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
@@ -1117,29 +1116,6 @@ __global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const double*
   if ((threadIdx.x & 31) == 0 && bal) atomicAdd(flags + F_N_DEGEN, __popc(bal));
 }
 
-// RHS landmark vector t = V+ b_l (normal_eq.py:221-226), lifted by B_lm in stage 2
-template <int STAGE>
-__global__ void k_lm_rhs_t(int n_l, const double* __restrict__ lbl,
-                           const double* __restrict__ lsys, const double* __restrict__ lrec,
-                           double* __restrict__ tarr) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= n_l) return;
-  const double* vs = lsys + (size_t)l * LSYS;
-  double P6[6] = {vs[0], vs[1], vs[2], vs[3], vs[4], vs[5]};
-  const double* bl = lbl + (size_t)l * 4;
-  double b3[3] = {bl[0], bl[1], bl[2]}, t[3];
-  sym3_apply(P6, b3, t);
-  if (STAGE == 1) {
-    st4(tarr + (size_t)l * 4, make_double4(t[0], t[1], t[2], 0.0));
-  } else {
-    const double* xp = lrec + (size_t)l * LREC;
-    double xv[4] = {xp[0], xp[1], xp[2], xp[3]}, h[4], t4[4];
-    householder_h<4>(xv, h);
-    basis_apply<4>(h, t, t4);
-    st4(tarr + (size_t)l * 4, make_double4(t4[0], t4[1], t4[2], t4[3]));
-  }
-}
-
 // camera vector for a gather pass: v = src (stage 1) or B src (stage 2)
 template <int STAGE>
 __global__ void k_setv(int n_p, const double* __restrict__ src, const double* __restrict__ ch,
@@ -1578,17 +1554,7 @@ __global__ void k_accept(int n_p, int n_l, const double* __restrict__ tcam,
   if (i < n_l) st4(lrec + (size_t)i * LREC, ld4(tlm + (size_t)i * 4));
 }
 
-// state upload helpers
-__global__ void k_put_state(int n_p, int n_l, const double* __restrict__ cams,
-                            const double* __restrict__ lms, double* __restrict__ crec,
-                            double* __restrict__ lrec) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_p)
-    for (int q = 0; q < 12; ++q) crec[(size_t)i * CREC + q] = cams[(size_t)i * 12 + q];
-  if (i < n_l)
-    for (int q = 0; q < 4; ++q) lrec[(size_t)i * LREC + q] = lms[(size_t)i * 4 + q];
-}
-
+// trial <- current copy (closed-form re-solve of the current state)
 __global__ void k_get_state(int n_p, int n_l, const double* __restrict__ crec,
                             const double* __restrict__ lrec, double* __restrict__ cams,
                             double* __restrict__ lms) {
