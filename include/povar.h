@@ -63,7 +63,8 @@ enum {
   PV_INFO_NP = 0, PV_INFO_NL_LOCAL = 1, PV_INFO_NO_LOCAL = 2, PV_INFO_TASKS = 3,
   PV_INFO_CHUNKS = 4, PV_INFO_LAUNCHES = 5, PV_INFO_RANK = 6, PV_INFO_WORLD = 7,
   PV_INFO_DEVICE_BYTES = 8, PV_INFO_NL_GLOBAL = 9, PV_INFO_RESOLVE_FALLBACKS = 10,
-  PV_INFO_BLOCKS = 11, PV_INFO_PERSIST_L2 = 12, PV_INFO_COUNT = 16
+  PV_INFO_BLOCKS = 11, PV_INFO_PERSIST_L2 = 12, PV_INFO_WARPS_PER_CAM = 13,
+  PV_INFO_COUNT = 16
 };
 
 /* tuning knobs of the term kernels (pv_set_option); results do not depend on them */

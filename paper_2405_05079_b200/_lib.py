@@ -19,7 +19,8 @@ PV_CURRENT, PV_TRIAL = 0, 1
 (PV_DBG_U, PV_DBG_UINV, PV_DBG_BP, PV_DBG_V, PV_DBG_VPINV, PV_DBG_BL, PV_DBG_DEGEN, PV_DBG_W,
  PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN) = range(12)
 INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
-               "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2")
+               "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2",
+               "warps_per_cam")
 PV_INFO_COUNT = 16
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
  PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE) = range(7)

@@ -77,6 +77,7 @@ struct pv_ctx {
   int64_t persist_l2 = 0;
   bool lm_lin_fresh = false;
   int num_sms = 148;
+  int wpc = 1;  // warps per camera in the camera kernels (from the mean segment size)
   int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
@@ -324,6 +325,12 @@ static void build_blocks(pv_ctx* c) {
   c->sync();
   c->blk_task = bt;
   c->n_blk = B;
+  {  // ~4 staged chunks per warp: warps per camera from the mean (camera, block) segment
+    const double mean_seg = (double)n_os / std::max<int64_t>(1, (int64_t)B * n_p);
+    int w = 1;
+    while (w < 8 && mean_seg > 4.0 * CH * w) w *= 2;
+    c->wpc = w;
+  }
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
@@ -449,9 +456,12 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca) {
                             CAM_SMEM));
     attr_set = true;
   }
-  k_cam<S, HC, EP, HA><<<blocks_for(c->n_p * 32, 256), 256, CAM_SMEM, c->stream>>>(
+  CamArgs a = ca;
+  a.wpc = c->wpc;
+  const int cams_per_cta = 8 / c->wpc;
+  k_cam<S, HC, EP, HA><<<blocks_for(c->n_p, cams_per_cta), 256, CAM_SMEM, c->stream>>>(
       c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->cyr, c->cbp, c->cUi, c->cx, c->crhs,
-      c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, ca);
+      c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, a);
   c->launched();
 }
 
@@ -478,6 +488,7 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
   a.term = term;
   a.check_stop = check_stop;
   a.project_y = 0;
+  a.wpc = 1;
   a.thr = thr;
   return a;
 }
@@ -725,6 +736,7 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_RESOLVE_FALLBACKS] = c->last_fallbacks;
   out[PV_INFO_BLOCKS] = c->n_blk;
   out[PV_INFO_PERSIST_L2] = c->persist_l2;
+  out[PV_INFO_WARPS_PER_CAM] = c->wpc;
   API_END(c)
 }
 

@@ -185,6 +185,7 @@ struct CamArgs {
   int term;         // term index for the stop test (EP_TERM)
   int check_stop;   // return immediately once the series has stopped
   int project_y;    // write the (stage-2 projected) y to cyr instead (schur apply)
+  int wpc;          // warps per camera (1, 2, 4, 8)
   double thr;
 };
 
@@ -196,16 +197,24 @@ __global__ void __launch_bounds__(256) k_cam(
     double* __restrict__ cx, double* __restrict__ crhs, const double* __restrict__ ch,
     double* __restrict__ nrm, PowerCtl* __restrict__ ctl, volatile PowerCtl* host_ctl,
     unsigned* __restrict__ ticket, Coef k, Tune tune, CamArgs ca) {
-  // one warp per camera; each (camera, block) segment is contiguous in memory
+  // ca.wpc warps per camera (1, 2, 4 or 8; 8 / wpc cameras per CTA).  The chunks of a
+  // (camera, block) segment are striped over the camera's warps; per-camera sums are
+  // combined in fixed order through shared memory.
   constexpr bool RHS = EP == EP_RHS;
   constexpr int D = STAGE == 1 ? 12 : 11;
   __shared__ bool last;
+  __shared__ double gred[8][12];
+  __shared__ double gv[8][12];
   extern __shared__ __align__(32) unsigned char cam_dsm[];
   if (ca.check_stop && ctl->stopped) return;  // grid-uniform
   const int lane = threadIdx.x & 31;
-  const int cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  unsigned char* wsm = cam_dsm + (size_t)(threadIdx.x >> 5) * CAM_WARP_SMEM;
+  const int warp = threadIdx.x >> 5;
+  const int wpc = ca.wpc;
+  const int grp = warp / wpc, gr = warp % wpc;
+  const int cam = blockIdx.x * (8 / wpc) + grp;
+  unsigned char* wsm = cam_dsm + (size_t)warp * CAM_WARP_SMEM;
   const bool valid = cam < g.n_p;
+  const bool leader = valid && gr == 0;
   const int np = g.n_p;
   const uint64_t pf = pol_sel(tune.pol_stream), pt = pol_sel(tune.pol_t),
                  ps = pol_sel(tune.pol_s);
@@ -216,25 +225,27 @@ __global__ void __launch_bounds__(256) k_cam(
     P1 = ldg4(cp + 4);
     P2v = ldg4(cp + 8);
   }
-  double yr = 0.0;  // lane r < 12: component r of this camera's y
-  if (HC && valid) {  // y_i (+)= sum_{j in blocks [c_lo, c_hi)} W_ij t_j
+  double yr = 0.0;  // leader lane r < 12: component r of this camera's y
+  if (HC) {  // y_i (+)= sum_{j in blocks [c_lo, c_hi)} W_ij t_j
     double acc[12];
 #pragma unroll
     for (int i = 0; i < 12; ++i) acc[i] = 0.0;
-    for (int b = ca.c_lo; b < ca.c_hi; ++b) {
+    for (int b = ca.c_lo; valid && b < ca.c_hi; ++b) {
       const int o_lo = __ldg(g.seg + (size_t)b * np + cam);
       const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
-      const int nch = (o_hi - o_lo + CH - 1) / CH;
-      if (nch > 0) stage_chunk(wsm, lane, o_lo, cs_x, g.cs_m, g.cs_lm);
+      const int nch_all = (o_hi - o_lo + CH - 1) / CH;
+      const int nch = nch_all > gr ? (nch_all - gr + wpc - 1) / wpc : 0;  // this warp's chunks
+      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
       cp_commit();
       for (int c = 0; c < nch; ++c) {
         unsigned char* buf = wsm + (c & 1) * CH_BUF;
-        if (c + 1 < nch) stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (c + 1) * CH, cs_x,
-                                     g.cs_m, g.cs_lm);
+        if (c + 1 < nch)
+          stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
+                      g.cs_m, g.cs_lm);
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        const int o0 = o_lo + c * CH;
+        const int o0 = o_lo + (gr + c * wpc) * CH;
         const double4* sx = reinterpret_cast<const double4*>(buf);
         const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
         const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
@@ -268,14 +279,25 @@ __global__ void __launch_bounds__(256) k_cam(
       cp_wait<0>();
     }
     warp_reduce_all(acc);
+    double mine = 0.0;
 #pragma unroll
     for (int i = 0; i < 12; ++i)
-      if (lane == i) yr = acc[i];
-    if (lane < 12) {  // fixed-order accumulation over blocks (deterministic)
+      if (lane == i) mine = acc[i];
+    if (wpc > 1) {  // fixed-order combination over the camera's warps
+      if (lane < 12) gred[warp][lane] = mine;
+      __syncthreads();
+      if (gr == 0 && lane < 12) {
+        double sacc = 0.0;
+        for (int q = 0; q < wpc; ++q) sacc += gred[warp + q][lane];
+        mine = sacc;
+      }
+    }
+    yr = mine;
+    if (leader && lane < 12) {  // fixed-order accumulation over blocks (deterministic)
       if (!ca.first_c) yr += cy[(size_t)cam * 12 + lane];
       cy[(size_t)cam * 12 + lane] = yr;
     }
-    if (ca.project_y) {  // schur apply: tangent projection (stage 2) -> cyr
+    if (ca.project_y && leader) {  // schur apply: tangent projection (stage 2) -> cyr
       double u = lane < 12 ? yr : 0.0;
       if (STAGE == 2) {
         const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
@@ -290,54 +312,57 @@ __global__ void __launch_bounds__(256) k_cam(
 
   double4 v0 = make_double4(0, 0, 0, 0), v1 = v0, v2 = v0;
   if (EP != EP_NONE) {
-    const bool row = lane < 12;
-    double u = 0.0;
-    if (row && valid) u = HC ? yr : cy[(size_t)cam * 12 + lane];
-    double h = 0.0;
-    if (STAGE == 2) {  // project y (12) -> tangent (11)
-      h = (row && valid) ? ch[(size_t)cam * 12 + lane] : 0.0;
-      const double hu = warp_sum(h * u);
-      const double pr = u - 2.0 * h * hu;
-      u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
-      if (lane >= 11) u = 0.0;
-    }
-    double vin = u;
-    if (RHS) {
-      const double b = (lane < D && valid) ? cbp[(size_t)cam * 12 + lane] : 0.0;
-      vin = lane < D ? -(b - u) : 0.0;
-      if (row && valid) crhs[(size_t)cam * 12 + lane] = vin;
-    }
-    double t = 0.0;
-    const double* Ui = cUi + (size_t)(valid ? cam : 0) * 144 + (lane < D ? lane : 0) * 12;
+    if (gr == 0) {  // leader warp of each camera (whole warp participates in shuffles)
+      const bool row = lane < 12;
+      double u = 0.0;
+      if (row && valid) u = HC ? yr : cy[(size_t)cam * 12 + lane];
+      double h = 0.0;
+      if (STAGE == 2) {  // project y (12) -> tangent (11)
+        h = (row && valid) ? ch[(size_t)cam * 12 + lane] : 0.0;
+        const double hu = warp_sum(h * u);
+        const double pr = u - 2.0 * h * hu;
+        u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
+        if (lane >= 11) u = 0.0;
+      }
+      double vin = u;
+      if (RHS) {
+        const double b = (lane < D && valid) ? cbp[(size_t)cam * 12 + lane] : 0.0;
+        vin = lane < D ? -(b - u) : 0.0;
+        if (row && valid) crhs[(size_t)cam * 12 + lane] = vin;
+      }
+      double t = 0.0;
+      const double* Ui = cUi + (size_t)(valid ? cam : 0) * 144 + (lane < D ? lane : 0) * 12;
 #pragma unroll
-    for (int kk = 0; kk < 12; ++kk) {
-      const double vk = __shfl_sync(PV_FULL, vin, kk);
-      if (valid && lane < D && kk < D) t = fma(Ui[kk], vk, t);
+      for (int kk = 0; kk < 12; ++kk) {
+        const double vk = __shfl_sync(PV_FULL, vin, kk);
+        if (valid && lane < D && kk < D) t = fma(Ui[kk], vk, t);
+      }
+      double xr = 0.0;
+      if (valid && lane < D) {
+        xr = RHS ? t : cx[(size_t)cam * 12 + lane] + t;
+        cx[(size_t)cam * 12 + lane] = xr;
+      }
+      double v = t;
+      if (STAGE == 2) {  // v = B t (11 -> 12)
+        const double tprev = __shfl_sync(PV_FULL, t, (lane + 31) & 31);
+        const double e = (lane >= 1 && lane < 12) ? tprev : 0.0;
+        const double hd = warp_sum(h * e);
+        v = e - 2.0 * h * hd;
+      }
+      if (row && valid) crec[(size_t)cam * CREC + 12 + lane] = v;  // for the later blocks
+      if (row) gv[grp][lane] = v;
+      const double tn = warp_sum(lane < D ? t * t : 0.0);
+      const double xn = warp_sum(lane < D ? xr * xr : 0.0);
+      if (lane == 0 && valid) {
+        nrm[2 * (size_t)cam] = tn;
+        nrm[2 * (size_t)cam + 1] = xn;
+      }
     }
-    double xr = 0.0;
-    if (valid && lane < D) {
-      xr = RHS ? t : cx[(size_t)cam * 12 + lane] + t;
-      cx[(size_t)cam * 12 + lane] = xr;
-    }
-    double v = t;
-    if (STAGE == 2) {  // v = B t (11 -> 12)
-      const double tprev = __shfl_sync(PV_FULL, t, (lane + 31) & 31);
-      const double e = (lane >= 1 && lane < 12) ? tprev : 0.0;
-      const double hd = warp_sum(h * e);
-      v = e - 2.0 * h * hd;
-    }
-    if (row && valid) crec[(size_t)cam * CREC + 12 + lane] = v;  // for the later blocks
-    v0 = make_double4(__shfl_sync(PV_FULL, v, 0), __shfl_sync(PV_FULL, v, 1),
-                      __shfl_sync(PV_FULL, v, 2), __shfl_sync(PV_FULL, v, 3));
-    v1 = make_double4(__shfl_sync(PV_FULL, v, 4), __shfl_sync(PV_FULL, v, 5),
-                      __shfl_sync(PV_FULL, v, 6), __shfl_sync(PV_FULL, v, 7));
-    v2 = make_double4(__shfl_sync(PV_FULL, v, 8), __shfl_sync(PV_FULL, v, 9),
-                      __shfl_sync(PV_FULL, v, 10), __shfl_sync(PV_FULL, v, 11));
-    const double tn = warp_sum(lane < D ? t * t : 0.0);
-    const double xn = warp_sum(lane < D ? xr * xr : 0.0);
-    if (lane == 0 && valid) {
-      nrm[2 * (size_t)cam] = tn;
-      nrm[2 * (size_t)cam + 1] = xn;
+    if (HA) {
+      __syncthreads();
+      v0 = make_double4(gv[grp][0], gv[grp][1], gv[grp][2], gv[grp][3]);
+      v1 = make_double4(gv[grp][4], gv[grp][5], gv[grp][6], gv[grp][7]);
+      v2 = make_double4(gv[grp][8], gv[grp][9], gv[grp][10], gv[grp][11]);
     }
   } else if (HA && valid) {
     const double* cp = crec + (size_t)cam * CREC + 12;
@@ -350,17 +375,19 @@ __global__ void __launch_bounds__(256) k_cam(
     for (int b = ca.a_lo; b < ca.a_hi; ++b) {
       const int o_lo = __ldg(g.seg + (size_t)b * np + cam);
       const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
-      const int nch = (o_hi - o_lo + CH - 1) / CH;
-      if (nch > 0) stage_chunk(wsm, lane, o_lo, cs_x, g.cs_m, g.cs_pos);
+      const int nch_all = (o_hi - o_lo + CH - 1) / CH;
+      const int nch = nch_all > gr ? (nch_all - gr + wpc - 1) / wpc : 0;
+      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_pos);
       cp_commit();
       for (int c = 0; c < nch; ++c) {
         unsigned char* buf = wsm + (c & 1) * CH_BUF;
-        if (c + 1 < nch) stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (c + 1) * CH, cs_x,
-                                     g.cs_m, g.cs_pos);
+        if (c + 1 < nch)
+          stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
+                      g.cs_m, g.cs_pos);
         cp_commit();
         cp_wait<1>();
         __syncwarp();
-        const int o0 = o_lo + c * CH;
+        const int o0 = o_lo + (gr + c * wpc) * CH;
         const double4* sx = reinterpret_cast<const double4*>(buf);
         const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
         const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
