@@ -467,13 +467,10 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca) {
 
 template <int S, int MODE>
 static void launch_lm_reduce(pv_ctx* c, int t_lo, int t_hi, int check_stop) {
-  // persistent pipelined warps: about three resident CTAs of 8 warps per SM
-  const int nt = t_hi - t_lo;
-  const int want = std::max(1, std::min(blocks_for((long long)nt * 32, 256),
-                                        c->num_sms * c->lr_ctas_per_sm));
-  k_lm_reduce<S, MODE><<<want, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
-                                                    c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
-                                                    c->tune, t_lo, t_hi, check_stop);
+  const int nb = blocks_for((long long)(t_hi - t_lo) * 32, 256);  // one task per warp
+  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
+                                                  c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
+                                                  c->tune, t_lo, t_hi, check_stop);
   c->launched();
 }
 

@@ -134,6 +134,18 @@ __device__ __forceinline__ void seg_reduce(double (&v)[N], int lane, int seg_end
   }
 }
 
+// Same, with only as many steps as the longest segment needs (max_len <= 32).
+template <int N>
+__device__ __forceinline__ void seg_reduce_n(double (&v)[N], int lane, int seg_end, int max_len) {
+  for (int d = 1; d < max_len; d <<= 1) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double o = __shfl_down_sync(PV_FULL, v[k], d);
+      if (lane + d < seg_end) v[k] += o;
+    }
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void warp_reduce_all(double (&v)[N]) {
 #pragma unroll

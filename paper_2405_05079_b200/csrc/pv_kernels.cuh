@@ -574,113 +574,85 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
   }
 }
 
-constexpr int LR_BATCH = 2;  // (non-pipelined launches) tasks per warp
-
-// per-task registers of the pipelined landmark reduce
-struct LrSlot {
-  Task t;
-  double4 sv;
-  LmPre pre;
-  int lm, send;
-  bool hd, valid;
-};
-
+// One landmark task per warp.  Lean on instructions (the kernel is issue-bound): only
+// the live components are reduced (3 in stage 1), the shuffle tree stops at the
+// task's longest segment, the heads' V+ loads are issued before the reduction.
 template <int STAGE, int MODE>
-__device__ __forceinline__ void lr_issue(const Graph& g, const double* __restrict__ sbuf,
-                                         const double* __restrict__ lrec,
-                                         const double* __restrict__ lsys,
-                                         const double* __restrict__ lbl, int4 d, bool valid,
-                                         int lane, uint64_t pf, LrSlot& sl) {
-  sl.valid = valid;
-  sl.t.o0 = d.x;
-  sl.t.n = d.y;
-  sl.t.l0 = d.z;
-  sl.t.heads = (unsigned)d.w;
-  sl.t.long_task = sl.t.n > 32;
-  sl.sv = make_double4(0.0, 0.0, 0.0, 0.0);
-  sl.hd = false;
-  sl.lm = sl.t.l0;
-  sl.send = 0;
-  if (!valid) return;
-  if (!sl.t.long_task) {
-    lane_segment(sl.t, lane, sl.lm, sl.send);
-    sl.hd = lane < sl.t.n && ((sl.t.heads >> lane) & 1u);
-    if (MODE != LR_RHS && lane < sl.t.n) sl.sv = ldg4p(sbuf + 4 * (size_t)(sl.t.o0 + lane), pf);
-  } else {
-    sl.hd = lane == 0;
-  }
-  if (sl.hd) sl.pre = lm_prefetch<STAGE, MODE>(sl.lm, lrec, lsys, lbl);
-}
-
-template <int STAGE, int MODE>
-__device__ __forceinline__ void lr_finish(const LrSlot& sl, int lane, double* __restrict__ sbuf,
-                                          double* __restrict__ tarr, double* __restrict__ ldl,
-                                          double* __restrict__ tlm, int* __restrict__ flags,
-                                          uint64_t pf, uint64_t pt, int discard) {
-  if (!sl.valid) return;
-  const Task& t = sl.t;
-  double acc[4] = {sl.sv.x, sl.sv.y, sl.sv.z, sl.sv.w};
-  if (t.long_task) {
-    if (MODE != LR_RHS) {
-      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-        const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
-        acc[0] += s.x;
-        acc[1] += s.y;
-        acc[2] += s.z;
-        acc[3] += s.w;
-      }
-      warp_reduce_all(acc);
-    }
-  } else if (MODE != LR_RHS) {
-    seg_reduce(acc, lane, sl.send);
-  }
-  if (sl.hd) lm_finish<STAGE, MODE>(sl.lm, acc, sl.pre, tarr, ldl, tlm, flags, pt);
-  if (MODE == LR_TERM && discard) {
-    // consumed partials are scratch: drop their L2 lines (only lines inside this task)
-    const size_t b0 = 4 * (size_t)t.o0 * sizeof(double);
-    const size_t b1 = 4 * (size_t)(t.o0 + t.n) * sizeof(double);
-    const size_t l0 = (b0 + 127) / 128, l1 = b1 / 128;
-    char* base = reinterpret_cast<char*>(sbuf);
-    for (size_t ln = l0 + lane; ln < l1; ln += 32)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + ln * 128) : "memory");
-  }
-}
-
-// Persistent, software-pipelined landmark reduce: each warp walks tasks
-// w, w + NW, w + 2 NW, ...; while task i reduces, the loads of task i + NW (s and
-// the heads' V+) and the descriptor of task i + 2 NW are already in flight.
-template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256, 3) k_lm_reduce(Graph g, double* __restrict__ sbuf,
-                                                      const double* __restrict__ lrec,
-                                                      double* __restrict__ tarr,
-                                                      const double* __restrict__ lsys,
-                                                      const double* __restrict__ lbl,
-                                                      double* __restrict__ ldl,
-                                                      double* __restrict__ tlm,
-                                                      const PowerCtl* __restrict__ ctl, int* flags,
-                                                      Tune tune, int task_lo, int task_hi,
-                                                      int check_stop) {
+__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__ sbuf,
+                                                   const double* __restrict__ lrec,
+                                                   double* __restrict__ tarr,
+                                                   const double* __restrict__ lsys,
+                                                   const double* __restrict__ lbl,
+                                                   double* __restrict__ ldl,
+                                                   double* __restrict__ tlm,
+                                                   const PowerCtl* __restrict__ ctl, int* flags,
+                                                   Tune tune, int task_lo, int task_hi,
+                                                   int check_stop) {
+  constexpr int NV = STAGE == 1 ? 3 : 4;
   const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  int ti = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (ti >= task_hi) return;
+  const int w = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (w >= task_hi) return;
   if (check_stop && ctl->stopped) return;
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
-  auto desc = [&](int i) {
-    return i < task_hi ? __ldg(g.task + i) : make_int4(0, 0, 0, 0);
-  };
-  LrSlot cur;
-  lr_issue<STAGE, MODE>(g, sbuf, lrec, lsys, lbl, desc(ti), true, lane, pf, cur);
-  int4 dn = desc(ti + nw);
-  while (true) {
-    const int tn = ti + nw;
-    LrSlot nxt;
-    lr_issue<STAGE, MODE>(g, sbuf, lrec, lsys, lbl, dn, tn < task_hi, lane, pf, nxt);
-    dn = desc(tn + nw);
-    lr_finish<STAGE, MODE>(cur, lane, sbuf, tarr, ldl, tlm, flags, pf, pt, tune.discard_s);
-    if (tn >= task_hi) break;
-    cur = nxt;
-    ti = tn;
+  const Task t = load_task(g, w, lane);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (t.long_task) {
+    const LmPre pre = lane == 0 ? lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl) : LmPre{};
+    if (MODE != LR_RHS) {
+      double a2[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) a2[i] = 0.0;
+#pragma unroll 4
+      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
+        const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
+        a2[0] += s.x;
+        a2[1] += s.y;
+        a2[2] += s.z;
+        if (NV == 4) a2[NV - 1] += s.w;
+      }
+      warp_reduce_all(a2);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = a2[i];
+    }
+    if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
+  } else {
+    int l, seg_end;
+    lane_segment(t, lane, l, seg_end);
+    const bool head = lane < t.n && ((t.heads >> lane) & 1u);
+    double a2[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a2[i] = 0.0;
+    if (MODE != LR_RHS && lane < t.n) {
+      const double4 s = ldg4p(sbuf + 4 * (size_t)(t.o0 + lane), pf);
+      a2[0] = s.x;
+      a2[1] = s.y;
+      a2[2] = s.z;
+      if (NV == 4) a2[NV - 1] = s.w;
+    }
+    LmPre pre;
+    if (head) pre = lm_prefetch<STAGE, MODE>(l, lrec, lsys, lbl);
+    if (MODE != LR_RHS) {
+      const unsigned len = head ? (unsigned)(seg_end - lane) : 1u;
+      const int max_len = (int)__reduce_max_sync(PV_FULL, len);
+      seg_reduce_n(a2, lane, seg_end, max_len);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = a2[i];
+    if (head) lm_finish<STAGE, MODE>(l, acc, pre, tarr, ldl, tlm, flags, pt);
+  }
+  if (MODE == LR_TERM && tune.discard_s) {
+    // the consumed partials are scratch: drop their L2 lines instead of writing them back
+    // (only lines entirely inside this task's observation range)
+    const unsigned l0 = (unsigned)((4ull * t.o0 * sizeof(double) + 127) / 128);
+    const unsigned l1 = (unsigned)((4ull * (t.o0 + t.n) * sizeof(double)) / 128);
+    if (l0 + lane < l1)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(sbuf) +
+                                                       (size_t)(l0 + lane) * 128)
+                   : "memory");
+    for (unsigned ln = l0 + 32 + lane; ln < l1; ln += 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(sbuf) +
+                                                       (size_t)ln * 128)
+                   : "memory");
   }
 }
 
