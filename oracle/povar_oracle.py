@@ -398,6 +398,65 @@ def power_solve(s: BlockSystem, max_order: int, threshold: float,
     return PowerResult(x, back_substitute(s, x), order, trunc, rhs, terms)
 
 
+def schur_diag_blocks(s: BlockSystem) -> np.ndarray:
+    """Exact block diagonal U_i - sum_j W_ij V+_j W_ij^T (normal_eq.py:253-260)."""
+    contrib = np.einsum("nij,njk,nlk->nil", s.W, s.V_pinv[s.g.lm], s.W)
+    return s.U - _seg_sum_cam(s.g, contrib)
+
+
+@dataclass
+class PcgResult:
+    pose_update: np.ndarray
+    landmark_update: np.ndarray
+    iterations: int
+    rel: float
+    flag: str | None
+    rhs: np.ndarray
+
+
+def pcg_solve(s: BlockSystem, max_iterations: int, tolerance: float) -> PcgResult:
+    """Block-Jacobi preconditioned CG on the reduced system (solvers.py:153-187)."""
+    rhs = schur_rhs(s)
+    rhs_norm = np.linalg.norm(rhs)
+    if rhs_norm == 0:
+        zero = np.zeros_like(rhs)
+        return PcgResult(zero, back_substitute(s, zero), 0, 0.0, None, rhs)
+    diag = schur_diag_blocks(s)
+    try:
+        m_inv = np.linalg.inv(diag)
+    except np.linalg.LinAlgError:
+        m_inv = pinv_psd(diag, 1e-12)[0]
+    n = s.g.n_cameras
+
+    def mapply(v):
+        return np.einsum("nij,nj->ni", m_inv, v.reshape(n, -1)).ravel()
+
+    x = np.zeros_like(rhs)
+    r = rhs.copy()
+    z = mapply(r)
+    p = z.copy()
+    rz = float(r @ z)
+    flag, iterations, rel = None, 0, 1.0
+    for it in range(1, max_iterations + 1):
+        iterations = it
+        sp = apply_schur(s, p)
+        curvature = float(p @ sp)
+        if curvature <= 0:
+            flag = "breakdown"
+            break
+        alpha = rz / curvature
+        x += alpha * p
+        r -= alpha * sp
+        rel = np.linalg.norm(r) / rhs_norm
+        if rel <= tolerance:
+            break
+        z = mapply(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return PcgResult(x, back_substitute(s, x), iterations, rel, flag, rhs)
+
+
 def tangent_trial(cams, lms, cam_bases, lm_bases, dx, dl):
     """Back-project, add, normalize; None on a zero norm (riemannian.py:110-122)."""
     n_p = len(cam_bases)
@@ -435,11 +494,17 @@ class StepResult:
 
 
 def lm_step(g: Graph, cams, lms, stage: int, lam: float, eta: float, max_order: int,
-            threshold: float, both: bool) -> StepResult:
-    """Linearize, assemble, power-solve and form the trial (solvers.py:349-367)."""
+            threshold: float, both: bool, inner: str = "power", max_inner: int = 500,
+            pcg_tol: float = 1e-6) -> StepResult:
+    """Linearize, assemble, inner-solve and form the trial (solvers.py:349-367)."""
     lin = linearize(g, cams, lms, stage, eta)
     sys_ = assemble(g, lin, lam, both or stage == 2)
-    pw = power_solve(sys_, max_order, threshold)
+    if inner == "power":
+        pw = power_solve(sys_, max_order, threshold)
+    elif inner == "pcg":
+        pw = pcg_solve(sys_, max_inner, pcg_tol)
+    else:
+        raise ValueError(f"unknown inner solver {inner!r}")
     if stage == 1:
         tc = cams + pw.pose_update.reshape(cams.shape)
         tl = np.array(lms, copy=True)
@@ -467,7 +532,7 @@ class LmLog:
 def lm_minimize(g: Graph, cams, lms, stage: int, *, max_iterations=50, ftol=1e-6,
                 lam0=1e-4, max_order=20, threshold=0.01, eta=0.1, varpro=True,
                 lam_inc=4.0, lam_dec=0.5, lam_min=1e-12, lam_max=1e8,
-                keep_states=False) -> LmLog:
+                keep_states=False, inner="power", max_inner=500, pcg_tol=1e-6) -> LmLog:
     """Levenberg-Marquardt outer loop (solvers.py:318-393)."""
     cams = np.array(cams, dtype=float)
     lms = np.array(lms, dtype=float)
@@ -480,9 +545,10 @@ def lm_minimize(g: Graph, cams, lms, stage: int, *, max_iterations=50, ftol=1e-6
     for _ in range(max_iterations):
         if keep_states:
             log.states.append((cams.copy(), lms.copy(), lam))
-        st = lm_step(g, cams, lms, stage, lam, eta, max_order, threshold, both)
+        st = lm_step(g, cams, lms, stage, lam, eta, max_order, threshold, both, inner,
+                     max_inner, pcg_tol)
         log.lambdas.append(lam)
-        log.orders.append(st.power.order_used)
+        log.orders.append(st.power.order_used if inner == "power" else st.power.iterations)
         log.f_trials.append(st.f_trial)
         f_trial = st.f_trial
         converged = False

@@ -16,6 +16,12 @@ tiny_lm.npz  -- BASELINE tiny config: reference stage-1 lm_minimize (20 its),
     first-iteration power solve, stage-2 lm_minimize from the lifted result
     (12 its) and its first riemannian_step.
 small_lm.npz -- BASELINE small config: reference stage-1 cost trace (50 its).
+pcg.npz      -- the PCG inner solver (solvers.py:153-187) on the mini graphs:
+    schur_diag_blocks and pcg_schur_solve at three (tolerance, cap) settings for
+    the stage-1 varpro / joint and stage-2 systems, plus lm_minimize traces with
+    inner_solver="pcg" (stage 1 and 2) on the mini graphs and the tiny config.
+
+``python tests/golden/make_golden.py pcg`` regenerates pcg.npz only.
 """
 
 from __future__ import annotations
@@ -201,7 +207,65 @@ def make_config_traces():
                                            float(state.cameras.sum())]))
 
 
+PCG_SETTINGS = (("t6", 1e-6, 500), ("t10", 1e-10, 5000), ("cap3", 1e-6, 3))
+
+
+def pcg_arrays(prefix, system):
+    out = {prefix + "diag": normal_eq.schur_diag_blocks(system)}
+    for tag, tol, cap in PCG_SETTINGS:
+        rep = solvers.pcg_schur_solve(system, solvers.SolverConfig(pcg_tolerance=tol,
+                                                                   max_inner_iterations=cap))
+        out[prefix + tag + "_dx"] = rep.pose_update
+        out[prefix + tag + "_dl"] = rep.landmark_update
+        out[prefix + tag + "_its"] = rep.inner_iterations_used
+        out[prefix + tag + "_rel"] = rep.truncation_estimate
+        out[prefix + tag + "_flag"] = rep.flag or ""
+    return out
+
+
+def make_pcg():
+    pose = objective.PoseConfig(0.1)
+    out = {}
+    for seed in range(3):
+        d = np.load(OUT / f"mini_{seed}.npz")
+        problem = stratba.BaProblem(int(d["n_cameras"]), int(d["n_landmarks"]),
+                                    len(d["cam_idx"]), d["cam_idx"].astype(np.int64),
+                                    d["lm_idx"].astype(np.int64), d["meas"])
+        st1 = stratba.ProjectiveState(d["cams"], d["lms"])
+        blocks = normal_eq.build_stage1_blocks(problem, st1, pose)
+        for lam, mode, tag in ((1e-4, normal_eq.POSE_ONLY, "s1v_"), (0.3, normal_eq.BOTH, "s1j_")):
+            out.update(pcg_arrays(f"m{seed}_{tag}", normal_eq.assemble(blocks, lam, mode)))
+        st2 = riemannian.retract(st1)
+        bases = riemannian.state_tangent_bases(st2)
+        raw = normal_eq.build_stage2_blocks(problem, st2)
+        system2 = normal_eq.assemble(riemannian.project_blocks(raw, bases), 1e-3, normal_eq.BOTH)
+        out.update(pcg_arrays(f"m{seed}_s2_", system2))
+        for tag, stage, state in (("lm1_", 1, st1), ("lm2_", 2, st2)):
+            cfg = solvers.SolverConfig(max_outer_iterations=10, inner_solver="pcg")
+            final, trace = solvers.lm_minimize(problem, state, stage, cfg)
+            out[f"m{seed}_{tag}costs"] = np.array([r.cost for r in trace.records])
+            out[f"m{seed}_{tag}cams"] = final.cameras
+            out[f"m{seed}_{tag}lms"] = final.landmarks
+    # tiny config, stage 1 with the iterative solver (20 its)
+    problem, _ = synth.make_problem("tiny", 0)
+    state = synth.random_state(problem, 1)
+    ref_problem = stratba.BaProblem(problem.num_cameras, problem.num_landmarks,
+                                    problem.num_observations, problem.camera_indices,
+                                    problem.landmark_indices, problem.measurements)
+    st = stratba.ProjectiveState(state.cameras, state.landmarks)
+    cfg = solvers.SolverConfig(max_outer_iterations=20, inner_solver="pcg")
+    t = time.time()
+    _, tr = solvers.lm_minimize(ref_problem, st, 1, cfg)
+    print("tiny stage1 pcg", time.time() - t)
+    out["tiny_lm1_costs"] = np.array([r.cost for r in tr.records])
+    np.savez_compressed(OUT / "pcg.npz", **out)
+
+
 if __name__ == "__main__":
     print("numpy", np.__version__)
-    make_mini()
-    make_config_traces()
+    if sys.argv[1:] == ["pcg"]:
+        make_pcg()
+    else:
+        make_mini()
+        make_config_traces()
+        make_pcg()

@@ -1,0 +1,107 @@
+"""CPU: the oracle's PCG inner solver (solvers.py:153-187) and exact block
+diagonal (normal_eq.py:253-260) against fixtures from the real reference
+(tests/golden/pcg.npz, made by tests/golden/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+from _pvutil import golden, rel
+from oracle import povar_oracle as O
+
+SETTINGS = (("t6", 1e-6, 500), ("t10", 1e-10, 5000), ("cap3", 1e-6, 3))
+
+
+@pytest.fixture(scope="module")
+def pcgz():
+    return golden("pcg.npz")
+
+
+def systems(seed):
+    z = golden(f"mini_{seed}.npz")
+    g = O.make_graph(int(z["n_cameras"]), int(z["n_landmarks"]), z["cam_idx"], z["lm_idx"],
+                     z["meas"])
+    lin1 = O.linearize(g, z["cams"], z["lms"], 1)
+    lin2 = O.linearize(g, z["cams2"], z["lms2"], 2)
+    return g, z, {"s1v_": O.assemble(g, lin1, 1e-4, False),
+                  "s1j_": O.assemble(g, lin1, 0.3, True),
+                  "s2_": O.assemble(g, lin2, 1e-3, True)}
+
+
+def check_pcg_result(dx, dl, its, rel_res, flag, pcgz, pre, st, tol, cap, x_dense):
+    """Parity rule for a CG solve (shared with the GPU tests).
+
+    Same iteration count and flag.  CG amplifies last-bit differences of S'.v
+    (1e-13 here) through the Krylov recursion, so two correct runs differ by a
+    fraction of the solve's own error: the update must agree to 1e-9 or to 5 % of
+    the reference's distance from the dense solution, whichever is larger.  The
+    final relative residual must meet the tolerance whenever the reference's did.
+    """
+    want_its = int(pcgz[pre + st + "_its"])
+    assert its == want_its, (pre, st, its, want_its)
+    assert (flag or "") == str(pcgz[pre + st + "_flag"])
+    err = rel(pcgz[pre + st + "_dx"], x_dense)
+    bound = max(1e-9, 0.05 * err)
+    assert rel(dx, pcgz[pre + st + "_dx"]) <= bound, (pre, st)
+    assert rel(dl, pcgz[pre + st + "_dl"]) <= 10 * bound, (pre, st)
+    want_rel = float(pcgz[pre + st + "_rel"])
+    if want_its < cap:
+        assert rel_res <= tol
+    else:
+        assert abs(rel_res - want_rel) <= 1e-6 * want_rel
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_pcg_and_diag_match_reference(pcgz, seed):
+    _, _, syss = systems(seed)
+    for tag, s in syss.items():
+        pre = f"m{seed}_{tag}"
+        # U - sum W V+ W^T cancels (stage 2 most): measured against the scale of U
+        assert (np.linalg.norm(O.schur_diag_blocks(s) - pcgz[pre + "diag"])
+                <= 1e-12 * np.linalg.norm(s.U)), tag
+        x_dense = np.linalg.solve(O.dense_reduced_matrix(s), O.schur_rhs(s))
+        for st, tol, cap in SETTINGS:
+            r = O.pcg_solve(s, cap, tol)
+            check_pcg_result(r.pose_update, r.landmark_update, r.iterations, r.rel, r.flag,
+                             pcgz, pre, st, tol, cap, x_dense)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("stage", [1, 2])
+def test_pcg_lm_traces_match_reference(pcgz, seed, stage):
+    _, z, _ = systems(seed)
+    g = O.make_graph(int(z["n_cameras"]), int(z["n_landmarks"]), z["cam_idx"], z["lm_idx"],
+                     z["meas"])
+    c, l = (z["cams"], z["lms"]) if stage == 1 else (z["cams2"], z["lms2"])
+    log = O.lm_minimize(g, c, l, stage, max_iterations=10, inner="pcg")
+    want = pcgz[f"m{seed}_lm{stage}_costs"]
+    assert len(log.costs) == len(want)
+    # same accept/reject pattern; costs within north_star's 1e-6 LM-trace tolerance
+    # (CG at pcg_tolerance 1e-6 passes last-bit differences on to the step)
+    assert [b < a for a, b in zip(log.costs, log.costs[1:])] == [
+        b < a for a, b in zip(want, want[1:])]
+    assert rel(log.costs, want) <= 1e-6
+
+
+def test_pcg_tiny_trace_matches_reference(pcgz):
+    from paper_2405_05079_b200 import synth
+    pr, _ = synth.make_problem("tiny", 0)
+    st = synth.random_state(pr, 1)
+    g = O.graph_of(pr)
+    log = O.lm_minimize(g, st.cameras, st.landmarks, 1, max_iterations=20, inner="pcg")
+    want = pcgz["tiny_lm1_costs"]
+    assert len(log.costs) == len(want)
+    assert rel(log.costs, want) <= 1e-6
+
+
+def test_pcg_matches_dense_solve_and_zero_rhs():
+    """test_solvers.py:120-139: PCG converges to the dense solve; zero RHS -> 0 iterations."""
+    g, z, syss = systems(1)
+    s = syss["s1v_"]
+    r = O.pcg_solve(s, 5000, 1e-12)
+    S = O.dense_reduced_matrix(s)
+    assert rel(r.pose_update, np.linalg.solve(S, r.rhs)) <= 1e-7  # cond(S) ~ 4e4
+    s.b_p[...] = 0.0
+    s.b_l[...] = 0.0
+    r0 = O.pcg_solve(s, 500, 1e-6)
+    assert r0.iterations == 0 and r0.rel == 0.0
+    assert not r0.pose_update.any()
