@@ -55,7 +55,9 @@ enum {
   PV_DBG_RHS = 8,      /* reduced RHS, n_p x 12                                          */
   PV_DBG_X = 9,        /* power-series pose update, n_p x 12                             */
   PV_DBG_DL = 10,      /* landmark update, n_ls x 3                                      */
-  PV_DBG_ULIN = 11     /* undamped (projected) U, n_p x 144                              */
+  PV_DBG_ULIN = 11,    /* undamped (projected) U, n_p x 144                              */
+  PV_DBG_SDIAG = 12,   /* exact Schur block diagonal of the last pv_pcg_solve, n_p x 144 */
+  PV_DBG_MINV = 13     /* its inverse (the block-Jacobi preconditioner), n_p x 144       */
 };
 
 /* info fields for pv_info */
@@ -124,6 +126,15 @@ int pv_damp(pv_ctx* ctx, double lam, int both, int64_t* n_degenerate);
 int pv_power_solve(pv_ctx* ctx, int max_order, double threshold, int* order_used,
                    double* truncation);
 
+/* pcg_schur_solve (solvers.py:153-187): block-Jacobi preconditioned CG on the
+ * reduced system, preconditioner = inverse of the exact block diagonal
+ * (schur_diag_blocks, normal_eq.py:253-260; np.linalg.inv with the
+ * _pinv_psd(., 1e-12) fallback).  Stops at relative residual <= tolerance or
+ * after max_iterations; *flag = 1 on non-positive curvature ("breakdown").
+ * Leaves the same device results as pv_power_solve (pv_get_step, pv_trial). */
+int pv_pcg_solve(pv_ctx* ctx, int max_iterations, double tolerance, int* iterations,
+                 double* relative_residual, int* flag);
+
 /* trial state (solvers.py:311-315 / riemannian.py:110-122); *ok = 0 when a
  * stage-2 norm collapses (apply_tangent_step returns None). */
 int pv_trial(pv_ctx* ctx, int stage, int* ok);
@@ -136,7 +147,7 @@ int pv_accept(pv_ctx* ctx, int stage, int resolve, double* f_new, int64_t* n_ran
  * fallback (solve_landmarks on the current state); result kept as current. */
 int pv_resolve_current(pv_ctx* ctx, int64_t* n_rank_deficient);
 
-/* StepReport arrays of the last pv_power_solve: dx (n_p*d), dl (n_l*dl) for the
+/* StepReport arrays of the last pv_power_solve / pv_pcg_solve: dx (n_p*d), dl (n_l*dl) for the
  * whole problem (unobserved / foreign-shard landmarks left untouched). */
 int pv_get_step(pv_ctx* ctx, double* dx, double* dl);
 

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpovar.so
 PV_OK, PV_EINVAL, PV_ECUDA, PV_ENCCL, PV_ENONFINITE, PV_EDEGENERATE = range(6)
 PV_CURRENT, PV_TRIAL = 0, 1
 (PV_DBG_U, PV_DBG_UINV, PV_DBG_BP, PV_DBG_V, PV_DBG_VPINV, PV_DBG_BL, PV_DBG_DEGEN, PV_DBG_W,
- PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN) = range(12)
+ PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN, PV_DBG_SDIAG, PV_DBG_MINV) = range(14)
 INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
                "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2",
                "warps_per_cam")
@@ -48,6 +48,9 @@ SIGNATURES = [
     ("pv_damp", ctypes.c_int, [_P, ctypes.c_double, ctypes.c_int, _I64]),
     ("pv_power_solve", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double,
                                       ctypes.POINTER(ctypes.c_int), _D]),
+    ("pv_pcg_solve", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double,
+                                    ctypes.POINTER(ctypes.c_int), _D,
+                                    ctypes.POINTER(ctypes.c_int)]),
     ("pv_trial", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("pv_accept", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _D, _I64]),
     ("pv_resolve_current", ctypes.c_int, [_P, _I64]),

@@ -18,6 +18,7 @@
 
 #include "../../include/povar.h"
 #include "pv_kernels.cuh"
+#include "pv_pcg.cuh"
 
 using namespace pv;
 
@@ -88,6 +89,10 @@ struct pv_ctx {
   unsigned* ticket;
   PowerCtl* ctl;
   PowerCtl* host_ctl = nullptr;  // mapped pinned mirror
+  // PCG (allocated on first use): moments, Schur diagonal, scratch, preconditioner,
+  // vectors x r z p sp, per-camera partials
+  double *cmom = nullptr, *csd = nullptr, *csdd = nullptr, *cmi = nullptr, *pvec = nullptr,
+         *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
   Tune tune{0, 1, 2, 2, 1};
@@ -555,6 +560,96 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   c->step_stage = S;
 }
 
+// K5 as apply_schur inside block-Jacobi PCG (solvers.py:153-187)
+template <int S>
+static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int* flag) {
+  const int D = S == 1 ? 12 : 11;
+  const size_t np = c->n_p;
+  if (!c->cmom) {
+    c->cmom = c->alloc<double>(np * 60);
+    c->csd = c->alloc<double>(np * 144);
+    c->csdd = c->alloc<double>(np * 144);
+    c->cmi = c->alloc<double>(np * 144);
+    c->pvec = c->alloc<double>(np * 12 * 4);
+    c->ppart = c->alloc<double>(np * 2);
+  }
+  PcgVec v{c->cx, c->pvec, c->pvec + np * 12, c->pvec + np * 24, c->pvec + np * 36};
+  const int B = c->n_blk;
+  const int wg = blocks_for((long long)np * 32, 256);  // one warp per camera
+  CK(cudaMemsetAsync(c->flags + F_SINGULAR_M, 0, 2 * sizeof(int), c->stream));
+  // K4: the reduced RHS (its U^-1 epilogue output is unused here)
+  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_tasks, 0);
+  launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, 0.0, 0);
+  // preconditioner: exact block diagonal and its inverse (solvers.py:161-166)
+  k_schur_diag<S><<<wg, 256, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->lsys, c->cmom, c->coef);
+  c->launched();
+  c->check_launch();
+  c->allreduce(c->cmom, np * 60);
+  k_diag_finish<S><<<wg, 256, 0, c->stream>>>((int)np, c->cmom, c->ch, c->cUd, c->csd);
+  k_damp_cam<<<blocks_for(np, 64), 64, 0, c->stream>>>((int)np, D, c->csd, 0.0, c->csdd, c->cmi,
+                                                       c->flags + (F_SINGULAR_M - F_SINGULAR_U));
+  c->launched(2);
+  c->check_launch();
+  int fl[F_COUNT];
+  CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (fl[F_SINGULAR_M]) {  // not positive definite: general inverse, then pinv
+    k_inv_lu<<<blocks_for(np, 32), 32, 0, c->stream>>>((int)np, D, c->csd, c->cmi, c->flags);
+    c->launched();
+    CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (fl[F_SINGULAR_M2]) {
+      k_pinv_jacobi<<<blocks_for(np, 32), 32, 0, c->stream>>>((int)np, D, c->csd, c->cmi);
+      c->launched();
+    }
+    c->check_launch();
+  }
+  k_pcg_init<S><<<wg, 256, 0, c->stream>>>((int)np, c->crhs, c->cmi, c->ch, c->crec, v, c->ppart,
+                                           c->ctl, c->host_ctl_dev, c->ticket);
+  c->launched();
+  c->check_launch();
+  c->sync();
+  // iterations with a one-iteration look-ahead on the device stop flag
+  for (int it = 1; it <= max_it && !((volatile PowerCtl*)c->host_ctl)->stopped; ++it) {
+    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 1));
+    for (int b = 0; b < B; ++b) {
+      launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 1);
+      if (b + 1 < B)
+        launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, 0, 0.0, 1));
+      else
+        launch_cam<S, true, EP_NONE, false>(c, cam_args(b, b + 1, b == 0, 0, 0, 0, 0.0, 1));
+    }
+    c->allreduce(c->cy, np * 12);
+    k_pcg_curv<S><<<wg, 256, 0, c->stream>>>((int)np, it, c->cy, c->ch, c->cUd, v, c->ppart,
+                                             c->ctl, c->host_ctl_dev, c->ticket);
+    k_pcg_update<S><<<wg, 256, 0, c->stream>>>((int)np, tol, c->cmi, v, c->ppart, c->ctl,
+                                               c->host_ctl_dev, c->ticket);
+    k_pcg_dir<S><<<wg, 256, 0, c->stream>>>((int)np, c->ch, c->crec, v, c->ctl);
+    c->launched(3);
+    CK(cudaEventRecord(c->ev[it & 1], c->stream));
+    if (it >= 2) {
+      CK(cudaEventSynchronize(c->ev[(it - 1) & 1]));
+      if (((volatile PowerCtl*)c->host_ctl)->stopped) break;
+    }
+  }
+  c->check_launch();
+  // K7 back-substitution with v = x
+  k_setv<S><<<blocks_for(np, 128), 128, 0, c->stream>>>((int)np, c->cx, c->ch, c->crec);
+  c->launched();
+  for (int b = 0; b < B; ++b) {
+    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0));
+    launch_lm_reduce<S, LR_BACKSUB>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+  }
+  c->check_launch();
+  PowerCtl h;
+  CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  *its = h.order;
+  *rel = h.trunc;
+  *flag = h.pad;
+  c->step_stage = S;
+}
+
 template <int S>
 static void op_trial(pv_ctx* c, int* ok) {
   k_trial_cam<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->crec, c->cx,
@@ -882,6 +977,21 @@ int pv_power_solve(pv_ctx* c, int max_order, double thr, int* order, double* tru
   API_END(c)
 }
 
+int pv_pcg_solve(pv_ctx* c, int max_iterations, double tolerance, int* iterations,
+                 double* relative_residual, int* flag) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (c->lin_stage == 0) throw PvError(PV_EINVAL, "pv_linearize first");
+  if (max_iterations < 0) throw PvError(PV_EINVAL, "max_iterations must be >= 0");
+  int its = 0, fl = 0;
+  double r = 0.0;
+  STAGE_DISPATCH(c->lin_stage, op_pcg, c, max_iterations, tolerance, &its, &r, &fl);
+  if (iterations) *iterations = its;
+  if (relative_residual) *relative_residual = r;
+  if (flag) *flag = fl;
+  API_END(c)
+}
+
 int pv_trial(pv_ctx* c, int stage, int* ok) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
@@ -1105,6 +1215,13 @@ int pv_debug_get(pv_ctx* c, int which, double* out) {
       cudaFree(w);
       c->allocs.pop_back();
       c->device_bytes -= std::max<size_t>((size_t)c->n_os * 36, 1) * 8;
+      break;
+    }
+    case PV_DBG_SDIAG:
+    case PV_DBG_MINV: {
+      if (!c->csd) throw PvError(PV_EINVAL, "no pv_pcg_solve yet");
+      auto h = down(which == PV_DBG_SDIAG ? c->csd : c->cmi, np * 144);
+      std::copy(h.begin(), h.end(), out);
       break;
     }
     default:

@@ -37,7 +37,7 @@ struct Tune {
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
-       F_N_FALLBACK = 5, F_COUNT = 8 };
+       F_N_FALLBACK = 5, F_SINGULAR_M = 6, F_SINGULAR_M2 = 7, F_COUNT = 8 };
 
 struct Graph {
   int n_p, n_l, n_o;
@@ -54,6 +54,8 @@ struct Graph {
   const double* cs_m;    // [n_o*2]
 };
 
+// stop / report state of the inner solve, shared by the power series and PCG
+// (PCG: order = iterations, trunc = relative residual, pad = 1 on breakdown)
 struct PowerCtl {
   int stopped;
   int order;
@@ -62,6 +64,7 @@ struct PowerCtl {
   double trunc;
   double xnorm;
   double tnorm;
+  double alpha, beta, rz, rhs_norm;  // PCG recurrences
 };
 
 struct Coef {

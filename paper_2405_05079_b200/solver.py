@@ -4,6 +4,8 @@ Mirrors the reference entry points on this path (pkg/src/stratba):
 
 * ``lm_minimize``        -> solvers.py:318-393  (PoVar / PoBA stage 1, RiPoBA stage 2)
 * ``power_schur_solve``  -> solvers.py:126-150  (on a device ``SchurSystem``)
+* ``pcg_schur_solve``    -> solvers.py:153-187  (block-Jacobi PCG, "iterative" / "ripcg")
+* ``solve_reduced``      -> solvers.py:251-260  (inner-solver dispatch: power | pcg)
 * ``riemannian_step``    -> riemannian.py:125-138
 * ``assemble_system``    -> normal_eq.py:62-89 + riemannian.py:67-85 + normal_eq.py:156-198
 * ``total_cost``         -> objective.py:194-211
@@ -131,6 +133,24 @@ class DeviceProblem:
                    ctypes.byref(trunc))
         return order.value, trunc.value
 
+    def pcg_solve(self, max_iterations: int, tolerance: float) -> tuple[int, float, str | None]:
+        its, rel_res, flag = ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        self._call("pv_pcg_solve", int(max_iterations), float(tolerance), ctypes.byref(its),
+                   ctypes.byref(rel_res), ctypes.byref(flag))
+        return its.value, rel_res.value, ("breakdown" if flag.value else None)
+
+    def inner_solve(self, config: SolverConfig) -> tuple[int, int, float, str | None]:
+        """solve_reduced (solvers.py:251-260) on the device system:
+        (inner_iterations_used, power_order_used, truncation_estimate, flag)."""
+        if config.inner_solver == "power":
+            order, trunc = self.power_solve(config.max_power_order, config.power_threshold)
+            return order, order, trunc, None
+        if config.inner_solver == "pcg":
+            its, rel_res, flag = self.pcg_solve(config.max_inner_iterations, config.pcg_tolerance)
+            return its, 0, rel_res, flag
+        raise NotImplementedError(
+            f"inner_solver={config.inner_solver!r}: the GPU path runs 'power' and 'pcg'")
+
     def trial(self, stage: int) -> bool:
         ok = ctypes.c_int()
         self._call("pv_trial", int(stage), ctypes.byref(ok))
@@ -171,7 +191,8 @@ class DeviceProblem:
                  _lib.PV_DBG_RHS: (self.n_p, 12), _lib.PV_DBG_X: (self.n_p, 12),
                  _lib.PV_DBG_V: (self.n_l_local, 6), _lib.PV_DBG_VPINV: (self.n_l_local, 6),
                  _lib.PV_DBG_BL: (self.n_l_local, 3), _lib.PV_DBG_DL: (self.n_l_local, 3),
-                 _lib.PV_DBG_DEGEN: (self.n_l_local,), _lib.PV_DBG_W: (self.n_o_local, 36)}
+                 _lib.PV_DBG_DEGEN: (self.n_l_local,), _lib.PV_DBG_W: (self.n_o_local, 36),
+                 _lib.PV_DBG_SDIAG: (self.n_p, 144), _lib.PV_DBG_MINV: (self.n_p, 144)}
         out = np.zeros(sizes[which])
         self._call("pv_debug_get", int(which), _lib.dptr(out))
         return out
@@ -280,6 +301,26 @@ def power_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
     return StepReport(dx, dl, order, order, trunc)
 
 
+def pcg_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
+    """solvers.py:153-187 on a device system (block-Jacobi PCG, exact diagonal blocks)."""
+    its, rel_res, flag = system.dp.pcg_solve(config.max_inner_iterations, config.pcg_tolerance)
+    dx, dl = system.dp.step(system.stage)
+    return StepReport(dx, dl, its, 0, rel_res, flag)
+
+
+_INNER_SOLVERS = {"power": power_schur_solve, "pcg": pcg_schur_solve}
+
+
+def solve_reduced(system: SchurSystem, config: SolverConfig) -> StepReport:
+    """Inner-solver dispatch (solvers.py:251-260).  ``direct`` (a sparse LU of the
+    materialised reduced matrix) is not part of the GPU path."""
+    fn = _INNER_SOLVERS.get(config.inner_solver)
+    if fn is None:
+        raise NotImplementedError(
+            f"inner_solver={config.inner_solver!r}: the GPU path runs 'power' and 'pcg'")
+    return fn(system, config)
+
+
 def riemannian_step(problem: BaProblem, state: ProjectiveState, config: SolverConfig,
                     lam: float | None = None, bases=None, *, dp: DeviceProblem | None = None
                     ) -> StepReport:
@@ -288,12 +329,10 @@ def riemannian_step(problem: BaProblem, state: ProjectiveState, config: SolverCo
     ``bases`` is accepted for signature compatibility; the device derives the
     same Householder bases (riemannian.py:37-56) from ``state``.
     """
-    if config.inner_solver != "power":
-        raise NotImplementedError("only the power-series inner solver runs on the GPU path")
     if lam is None:
         lam = config.initial_lambda
     system = assemble_system(problem, state, STAGE2, lam, BOTH, config.pose, dp=dp)
-    return power_schur_solve(system, config)
+    return solve_reduced(system, config)
 
 
 def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: SolverConfig,
@@ -310,9 +349,9 @@ def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: 
     """
     if stage not in (STAGE1, STAGE2):
         raise ValueError(f"unknown stage {stage!r}")
-    if config.inner_solver != "power":
+    if config.inner_solver not in _INNER_SOLVERS:
         raise NotImplementedError(
-            f"inner_solver={config.inner_solver!r}: only the power series runs on the GPU path")
+            f"inner_solver={config.inner_solver!r}: the GPU path runs 'power' and 'pcg'")
     pose = config.pose
     dp = dp or device_problem(problem, pose.eta)
     dp.set_state(state)
@@ -334,7 +373,7 @@ def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: 
             dp.linearize(stage)  # FloatingPointError on a degenerate stage-2 point
             linearized = True
         dp.damp(lam, both)
-        order, _trunc = dp.power_solve(config.max_power_order, config.power_threshold)
+        its, order, _trunc, _flag = dp.inner_solve(config)
         ok = dp.trial(stage)
         f_trial = dp.cost(stage, trial=True) if ok else math.inf
         converged = False
@@ -354,7 +393,7 @@ def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: 
             lam = min(config.lambda_max, lam * config.lambda_increase)
         if decisions is not None:
             decisions.append(dict(iteration=it, f_trial=f_trial, accepted=accepted, order=order,
-                                  lam_next=lam))
+                                  inner_iterations=its, lam_next=lam))
         rec = TraceRecord(it, f, time.perf_counter() - t0)
         records.append(rec)
         if trace_sink is not None:
