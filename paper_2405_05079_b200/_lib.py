@@ -59,6 +59,15 @@ SIGNATURES = [
     ("pv_bench_terms", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_float)]),
     ("pv_debug_get", ctypes.c_int, [_P, ctypes.c_int, _D]),
+    # include/povar_bal.h (host-only BAL input path)
+    ("pv_bal_header", ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, _I64, _I64, _I64, _I64,
+                                     ctypes.c_char_p, ctypes.c_size_t]),
+    ("pv_bal_parse", ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, _I64, _I64,
+                                    _D, _D, _D, _I64, ctypes.c_char_p, ctypes.c_size_t]),
+    ("pv_bal_prune_masks", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I64,
+                                          _I64, ctypes.c_int64,
+                                          ctypes.POINTER(ctypes.c_uint8),
+                                          ctypes.POINTER(ctypes.c_uint8), _I64]),
 ]
 
 _lib = None

@@ -21,7 +21,15 @@ pcg.npz      -- the PCG inner solver (solvers.py:153-187) on the mini graphs:
     the stage-1 varpro / joint and stage-2 systems, plus lm_minimize traces with
     inner_solver="pcg" (stage 1 and 2) on the mini graphs and the tiny config.
 
-``python tests/golden/make_golden.py pcg`` regenerates pcg.npz only.
+bal_cases.json -- parse_bal outcomes (arrays or BalParseError line + message) on
+    hand-written texts covering the token grammar and every error path.
+tiny.bal.gz  -- the tiny config written by the reference's write_bal (parser and
+    pipeline input); prune.npz -- prune_underobserved on a graph with single,
+    duplicate-camera and unobserved landmarks and an empty camera.
+pipeline_*   -- run_problem summaries / trace CSVs on tiny.bal.gz
+    (povar + ripoba full, iterative stage 1).
+
+``python tests/golden/make_golden.py pcg|bal`` regenerates one group only.
 """
 
 from __future__ import annotations
@@ -261,11 +269,117 @@ def make_pcg():
     np.savez_compressed(OUT / "pcg.npz", **out)
 
 
+BAL_TEXTS = {
+    "basic": "2 3 4\n0 0 1.5 -2\n1 0 3e-1 4E+2\n0 1 5 6\n1 2 7 8\n"
+             + "1 2 3 4 5 6 7 8 9\n" * 2 + "0.1 0.2 0.3\n" * 3,
+    "whitespace": "2\t3  4\r\n0 0\r1.5 -2 1 0\v3e-1\f4E+2\n\n0 1 5 6 1 2 7\u00a08\n"
+                  + " ".join(["1"] * 18) + "\r\n" + " ".join(["0.5"] * 9) + "\n",
+    "syntax": "+2 0_3 004\n00 0_1 1_000.5 .5\n1 0 5. -.25e-1_0\n0 1 1e-400 1e400\n"
+              "1 2 inf -Infinity\n" + "1 2 3 4 5 6 7 8 9\n" * 2 + "0.1 0.2 0.3\n" * 3,
+    "empty": "",
+    "header_float": "2.0 3 4\n",
+    "header_negative": "2 -3 4\n",
+    "header_truncated": "2 3",
+    "cam_range": "2 3 1\n2 0 1 1\n",
+    "pt_range": "2 3 1\n\n1 -1 1 1\n",
+    "big_index": "2 3 1\n99999999999999999999 0 1 1\n",
+    "int_as_float": "2 3 1\n1e0 0 1 1\n",
+    "bad_underscore": "2 3 1\n1__0 0 1 1\n",
+    "bad_meas": "2 3 1\n1 0 abc 1\n",
+    "quote_token": "2 3 1\n1 0 1 a'b\n",
+    "obs_truncated": "2 3 2\n1 0 1 1\n0 1\n",
+    "cam_truncated": "1 1 1\n0 0 1 1\n1 2 3\n",
+    "pt_truncated": "1 1 1\n0 0 1 1\n1 2 3 4 5 6 7 8 9\n1 2\n",
+    "trailing": "1 1 1\n0 0 1 1\n1 2 3 4 5 6 7 8 9\n1 2 3\n\n4\n",
+    "bad_cam_param": "1 1 1\n0 0 1 1\n1 2 3 4 x 6 7 8 9\n1 2 3\n",
+    "hex_float": "1 1 1\n0 0 0x1p3 1\n",
+}
+
+
+def make_bal():
+    import gzip
+    import io
+    import json
+    from stratba import bal_io
+    cases = []
+    for name, text in BAL_TEXTS.items():
+        try:
+            p = bal_io.parse_bal(io.StringIO(text))
+            out = {"ok": {"n": [p.num_cameras, p.num_landmarks, p.num_observations],
+                          "cam": p.camera_indices.tolist(), "pt": p.landmark_indices.tolist(),
+                          "meas": [[repr(float(v)) for v in r] for r in p.measurements],
+                          "cams": [[repr(float(v)) for v in r] for r in p.metric_cameras],
+                          "pts": [[repr(float(v)) for v in r] for r in p.metric_points]}}
+        except bal_io.BalParseError as exc:
+            out = {"error": [exc.line, str(exc)]}
+        cases.append({"name": name, "text": text, **out})
+    with open(OUT / "bal_cases.json", "w") as fh:
+        json.dump(cases, fh, indent=1)
+    # tiny config through the reference writer
+    problem, _ = synth.make_problem("tiny", 0)
+    ref_problem = stratba.BaProblem(problem.num_cameras, problem.num_landmarks,
+                                    problem.num_observations, problem.camera_indices,
+                                    problem.landmark_indices, problem.measurements)
+    buf = io.StringIO()
+    bal_io.write_bal(ref_problem, buf)
+    with gzip.GzipFile(OUT / "tiny.bal.gz", "wb", mtime=0) as fh:
+        fh.write(buf.getvalue().encode())
+    # pruning: singles, a duplicate-camera landmark, an unobserved landmark, an empty camera
+    rng = np.random.default_rng(7)
+    ci, li = [], []
+    for j in range(40):
+        kind = j % 5
+        if kind == 0:      # single observation
+            cams = [int(rng.integers(0, 6))]
+        elif kind == 1:    # same camera twice
+            c = int(rng.integers(0, 6))
+            cams = [c, c]
+        elif kind == 2:    # unobserved
+            cams = []
+        else:
+            cams = sorted(rng.choice(6, size=int(rng.integers(2, 5)), replace=False).tolist())
+        for c in cams:
+            ci.append(c)
+            li.append(j)
+    ci = np.array(ci)
+    ci[ci == 4] = 5  # camera 4 only ever sees pruned landmarks / nothing
+    perm = rng.permutation(len(ci))
+    meas = rng.standard_normal((len(ci), 2))
+    raw = stratba.BaProblem(7, 40, len(ci), ci[perm], np.array(li)[perm], meas,
+                            rng.standard_normal((7, 9)), rng.standard_normal((40, 3)))
+    pr = bal_io.prune_underobserved(raw)
+    np.savez_compressed(OUT / "prune.npz", cam_idx=raw.camera_indices, lm_idx=raw.landmark_indices,
+                        meas=raw.measurements, cams=raw.metric_cameras, pts=raw.metric_points,
+                        p_n=np.array([pr.num_cameras, pr.num_landmarks, pr.num_observations]),
+                        p_cam=pr.camera_indices, p_lm=pr.landmark_indices, p_meas=pr.measurements,
+                        p_cams=pr.metric_cameras, p_pts=pr.metric_points)
+    # the pipeline on tiny.bal.gz
+    import shutil
+    import tempfile
+    from stratba import pipeline
+    # seed 0 / 30 iterations: a stage-1 result converged enough for a well-conditioned
+    # stage 2 (the oracle reproduces this chain within 3e-11); the PCG chain is
+    # tolerance-limited, so its fixture covers stage 1 only
+    for tag, stage, s1, s2, its in (("povar", "full", "povar", "ripoba", 30),
+                                    ("iterative", "stage1", "iterative", "ripcg", 20)):
+        with tempfile.TemporaryDirectory() as td:
+            spec = pipeline.RunSpec(inputs=[str(OUT / "tiny.bal.gz")], seed=0, stage=stage,
+                                    stage1_solver=s1, stage2_solver=s2, max_iterations=its,
+                                    out_dir=td)
+            pipeline.run_problem(OUT / "tiny.bal.gz", spec)
+            shutil.copy(Path(td) / "tiny_summary.json", OUT / f"pipeline_{tag}_summary.json")
+            shutil.copy(Path(td) / "tiny_trace.csv", OUT / f"pipeline_{tag}_trace.csv")
+        print("pipeline", tag)
+
+
 if __name__ == "__main__":
     print("numpy", np.__version__)
     if sys.argv[1:] == ["pcg"]:
         make_pcg()
+    elif sys.argv[1:] == ["bal"]:
+        make_bal()
     else:
         make_mini()
         make_config_traces()
         make_pcg()
+        make_bal()

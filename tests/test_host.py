@@ -47,9 +47,9 @@ def test_trace_and_labels():
 
 
 def test_header_symbols_are_bound_and_exported():
-    """Every entry point declared in include/povar.h is exported by libpovar.so and bound."""
+    """Every entry point declared in include/*.h is exported by libpovar.so and bound."""
     from paper_2405_05079_b200 import _lib
-    header = (ROOT / "include" / "povar.h").read_text()
+    header = "".join(p.read_text() for p in sorted((ROOT / "include").glob("*.h")))
     declared = set(re.findall(r"\b(pv_[a-z_0-9]+)\s*\(", header))
     bound = {name for name, _, _ in _lib.SIGNATURES}
     assert declared == bound, declared ^ bound
