@@ -797,8 +797,10 @@ __global__ void __launch_bounds__(256) k_lin_lm(Graph g, const double* __restric
       double2 m = ldg2(g.ls_m + 2 * (size_t)o);
       lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, k, acc, flags);
     }
-    seg_reduce(acc, lane, seg_end);
-    if (lane < t.n && ((t.heads >> lane) & 1u)) lin_lm_finish<STAGE>(l, acc, x, lvr, lbl);
+    const bool head = lane < t.n && ((t.heads >> lane) & 1u);
+    seg_reduce_n(acc, lane, seg_end,
+                 (int)__reduce_max_sync(PV_FULL, head ? (unsigned)(seg_end - lane) : 1u));
+    if (head) lin_lm_finish<STAGE>(l, acc, x, lvr, lbl);
   }
 }
 
@@ -1417,6 +1419,9 @@ __global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __rest
     }
     const bool head = t.long_task ? lane == 0 : (lane < t.n && ((t.heads >> lane) & 1u));
     const int oend = t.o0 + t.n;
+    // shuffle steps the longest segment of a short task needs (results identical)
+    const int max_len =
+        t.long_task ? 32 : (int)__reduce_max_sync(PV_FULL, head ? (unsigned)(seg_end - lane) : 1u);
     // short tasks keep their single observation's rows in registers for all passes
     Rows4 mine;
     const bool have = !t.long_task && lane < t.n;
@@ -1435,7 +1440,7 @@ __global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __rest
       warp_reduce_all(g1);
     } else {
       if (have) gram6(mine, g1);
-      seg_reduce(g1, lane, seg_end);
+      seg_reduce_n(g1, lane, seg_end, max_len);
     }
     double R1[6] = {0, 0, 0, 0, 0, 0};
     double fb = 0.0;  // 0: normal equations suffice, 1: CholeskyQR2 pass, 2: Givens fallback
@@ -1462,7 +1467,7 @@ __global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __rest
     }
     if (need2) {
       if (t.long_task) warp_reduce_all(s2);
-      else seg_reduce(s2, lane, seg_end);
+      else seg_reduce_n(s2, lane, seg_end, max_len);
     }
     double xn[4] = {0.0, 0.0, 0.0, 0.0};
     if (head) {
