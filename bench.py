@@ -197,6 +197,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stage2", action="store_true")
+    ap.add_argument("--no-pcg", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -309,6 +310,28 @@ def main():
                 "peak_source": peak_src,
                 "note": "achieved/traffic per term (summed over the landmark-block launches)"}
 
+    # ---- PCG inner solver ("iterative", solvers.py:153-187) on the same system -----
+    pcg = None
+    if not args.no_pcg:
+        dp.linearize(1)
+        dp.damp(lam, False)
+        dp.pcg_solve(2, 1e-300)  # warm
+        tms = {}
+        for n_it in (1, 21):  # tolerance 0 -> exactly n_it iterations
+            barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            its, _, _ = dp.pcg_solve(n_it, 1e-300)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tms[n_it] = max_over_ranks(a.elapsed_time(b))
+        per_it = (tms[21] - tms[1]) / 20
+        pcg = {"ms_per_iteration": per_it, "ms_setup_plus_one_iteration": tms[1],
+               "ms_21_iterations": tms[21],
+               "note": "RHS + exact Schur block diagonal + its inverse + back-substitution are "
+                       "the setup; one iteration = one blocked S'.p term + 3 vector kernels"}
+
     # ---- stage 2 (RiPoBA) iteration throughput from the lifted state ------------
     stage2 = None
     if not args.no_stage2:
@@ -402,7 +425,7 @@ def main():
                            "parallelism": f"landmark-sharded dp{world}"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(), "spmv": spmv,
-                "stage2": stage2}
+                "stage2": stage2, "pcg": pcg}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
