@@ -677,10 +677,14 @@ __global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __
 // ---------------------------------------------------------------------------
 // K1 + K2 (landmark side of the linearization): V = sum Jl^T Jl, b_l = sum Jl^T r
 
+// V (6 unique) and b_l (3) of one observation, in the landmark's tangent space:
+// stage 1 J_l rows are already 3-wide; stage 2 rows (2x4) are projected with the
+// Householder basis of x first (riemannian.py:67-85 projects the blocks before
+// normal_eq.py:156-198 assembles), so both stages reduce 9 values.
 template <int STAGE>
 __device__ __forceinline__ void lin_lm_obs(const double* __restrict__ crec, int cam, double m0,
-                                           double m1, const double4& x, const Coef& k,
-                                           double (&acc)[14], int* flags) {
+                                           double m1, const double4& x, const double (&h)[4],
+                                           const Coef& k, double (&acc)[9], int* flags) {
   const double* c = crec + (size_t)cam * CREC;
   double4 P0 = ldg4(c), P1 = ldg4(c + 4), P2 = ldg4(c + 8);
   double u0 = dot4(P0, x), u1 = dot4(P1, x), u2 = dot4(P2, x);
@@ -717,55 +721,27 @@ __device__ __forceinline__ void lin_lm_obs(const double* __restrict__ crec, int 
     double rr[2] = {u0 / u2 - m0, u1 / u2 - m1};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      int e = 0;
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = a; b < 4; ++b) {
-          acc[e] = fma(J[q][a], J[q][b], acc[e]);
-          ++e;
-        }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) acc[10 + a] = fma(J[q][a], rr[q], acc[10 + a]);
+      double jt[3];
+      basis_apply_t<4>(h, J[q], jt);  // J_l B (riemannian.py:80-82)
+      acc[0] = fma(jt[0], jt[0], acc[0]);
+      acc[1] = fma(jt[0], jt[1], acc[1]);
+      acc[2] = fma(jt[0], jt[2], acc[2]);
+      acc[3] = fma(jt[1], jt[1], acc[3]);
+      acc[4] = fma(jt[1], jt[2], acc[4]);
+      acc[5] = fma(jt[2], jt[2], acc[5]);
+      acc[6] = fma(jt[0], rr[q], acc[6]);
+      acc[7] = fma(jt[1], rr[q], acc[7]);
+      acc[8] = fma(jt[2], rr[q], acc[8]);
     }
   }
 }
 
-template <int STAGE>
-__device__ __forceinline__ void lin_lm_finish(int l, const double (&acc)[14], const double4& x,
+__device__ __forceinline__ void lin_lm_finish(int l, const double (&acc)[9],
                                               double* __restrict__ lvr, double* __restrict__ lbl) {
-  double V6[6], b3[3];
-  if (STAGE == 1) {
-    for (int i = 0; i < 6; ++i) V6[i] = acc[i];
-    for (int i = 0; i < 3; ++i) b3[i] = acc[6 + i];
-  } else {  // riemannian.py:67-85: B^T V B, B^T b with the Householder basis of x
-    double xv[4] = {x.x, x.y, x.z, x.w}, h[4];
-    householder_h<4>(xv, h);
-    double V[4][4];
-    int e = 0;
-    for (int a = 0; a < 4; ++a)
-      for (int b = a; b < 4; ++b) {
-        V[a][b] = acc[e];
-        V[b][a] = acc[e];
-        ++e;
-      }
-    double w[4], al = 0.0;
-    for (int a = 0; a < 4; ++a) {
-      w[a] = V[a][0] * h[0] + V[a][1] * h[1] + V[a][2] * h[2] + V[a][3] * h[3];
-      al = fma(h[a], w[a], al);
-    }
-    e = 0;
-    for (int a = 1; a < 4; ++a)
-      for (int b = a; b < 4; ++b) {
-        V6[e++] = V[a][b] - 2.0 * h[a] * w[b] - 2.0 * w[a] * h[b] + 4.0 * al * h[a] * h[b];
-      }
-    double bb[4] = {acc[10], acc[11], acc[12], acc[13]};
-    basis_apply_t<4>(h, bb, b3);
-  }
   double* o = lvr + (size_t)l * 8;
-  st4(o, make_double4(V6[0], V6[1], V6[2], V6[3]));
-  st4(o + 4, make_double4(V6[4], V6[5], 0.0, 0.0));
-  st4(lbl + (size_t)l * 4, make_double4(b3[0], b3[1], b3[2], 0.0));
+  st4(o, make_double4(acc[0], acc[1], acc[2], acc[3]));
+  st4(o + 4, make_double4(acc[4], acc[5], 0.0, 0.0));
+  st4(lbl + (size_t)l * 4, make_double4(acc[6], acc[7], acc[8], 0.0));
 }
 
 template <int STAGE>
@@ -777,30 +753,39 @@ __global__ void __launch_bounds__(256) k_lin_lm(Graph g, const double* __restric
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= g.n_tasks) return;
   Task t = load_task(g, w, lane);
-  double acc[14];
+  double acc[9];
 #pragma unroll
-  for (int i = 0; i < 14; ++i) acc[i] = 0.0;
+  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
+  double h[4] = {0.0, 0.0, 0.0, 0.0};
   if (t.long_task) {
     double4 x = ldg4(lrec + (size_t)t.l0 * LREC);
+    if (STAGE == 2) {
+      const double xv[4] = {x.x, x.y, x.z, x.w};
+      householder_h<4>(xv, h);
+    }
     for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
       double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, k, acc, flags);
+      lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, h, k, acc, flags);
     }
     warp_reduce_all(acc);
-    if (lane == 0) lin_lm_finish<STAGE>(t.l0, acc, x, lvr, lbl);
+    if (lane == 0) lin_lm_finish(t.l0, acc, lvr, lbl);
   } else {
     int l, seg_end;
     lane_segment(t, lane, l, seg_end);
     double4 x = ldg4(lrec + (size_t)l * LREC);
+    if (STAGE == 2) {
+      const double xv[4] = {x.x, x.y, x.z, x.w};
+      householder_h<4>(xv, h);
+    }
     if (lane < t.n) {
       int o = t.o0 + lane;
       double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-      lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, k, acc, flags);
+      lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, h, k, acc, flags);
     }
     const bool head = lane < t.n && ((t.heads >> lane) & 1u);
     seg_reduce_n(acc, lane, seg_end,
                  (int)__reduce_max_sync(PV_FULL, head ? (unsigned)(seg_end - lane) : 1u));
-    if (head) lin_lm_finish<STAGE>(l, acc, x, lvr, lbl);
+    if (head) lin_lm_finish(l, acc, lvr, lbl);
   }
 }
 
