@@ -82,12 +82,56 @@ def _worker(rank, world, port, q):
         # cost partials -> allreduce (povar.cu op_cost)
         f = allreduce(np.array([O.total_cost(g_loc, st.cameras, st.landmarks, 1)]))[0]
         ok.append(abs(f - O.total_cost(g_all, st.cameras, st.landmarks, 1)) <= 1e-12 * f)
+        # PCG (povar.cu op_pcg): the block-diagonal moments and every S'.p partial are
+        # allreduced; the CG recurrences run replicated on the reduced camera vectors
+        full = ref
+        U_d = O.jacobi_damp(U_sum, lam)
+        contrib = allreduce(loc.U - O.schur_diag_blocks(loc))
+        m_inv = np.linalg.inv(U_d - contrib)
+        b_l_part = loc.b_l  # landmark-local
+        rhs = -(bp_sum.ravel() - allreduce(O.w_apply(loc, np.einsum("nij,nj->ni", loc.V_pinv,
+                                                                      b_l_part)).ravel()))
+        n = pr.num_cameras
+
+        def mapply(M, v):
+            return np.einsum("nij,nj->ni", M, v.reshape(n, -1)).ravel()
+
+        x = np.zeros_like(rhs)
+        r = rhs.copy()
+        z = mapply(m_inv, r)
+        p = z.copy()
+        rz = float(r @ z)
+        its = 0
+        rhs_norm = np.linalg.norm(rhs)
+        for it in range(1, 200):
+            its = it
+            sp = mapply(U_d, p) - allreduce(O.coupling(loc, p))
+            alpha = rz / float(p @ sp)
+            x += alpha * p
+            r -= alpha * sp
+            if np.linalg.norm(r) / rhs_norm <= 1e-8:
+                break
+            z = mapply(m_inv, r)
+            rz_new = float(r @ z)
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        want = O.pcg_solve(full, 199, 1e-8)
+        ok.append(abs(its - want.iterations) <= 1)
+        ok.append(np.linalg.norm(x - want.pose_update) <= 1e-6 * np.linalg.norm(want.pose_update))
+        got = torch.tensor([float(its)], dtype=torch.float64)
+        mx, mn = got.clone(), got.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        ok.append(float(mx) == float(mn))  # identical stop decision on every rank
         # NCCL id broadcast used to build the device communicator
         nid = shard.broadcast_nccl_id(rank, world)
         ids = [None] * world
         dist.all_gather_object(ids, nid)
         ok.append(len(nid) == 128 and all(i == ids[0] for i in ids))
         q.put((rank, ok, plan))
+    except Exception as exc:  # report instead of leaving the parent waiting on the queue
+        q.put((rank, [repr(exc)], None))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -106,5 +150,5 @@ def test_two_rank_shard_partials_allreduce():
         p.join(timeout=60)
         assert p.exitcode == 0
     for rank, ok, plan in results:
-        assert all(ok), (rank, ok)
+        assert all(isinstance(x, (bool, np.bool_)) and x for x in ok), (rank, ok)
     assert results[0][2] == results[1][2]
