@@ -12,7 +12,9 @@ import os
 
 from .types import NumericFailureError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpovar.so")
+# PV_LIB_PATH: an alternative build of the same library (tuning experiments, tools/)
+LIB_PATH = os.environ.get("PV_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libpovar.so")
 
 PV_OK, PV_EINVAL, PV_ECUDA, PV_ENCCL, PV_ENONFINITE, PV_EDEGENERATE = range(6)
 PV_CURRENT, PV_TRIAL = 0, 1
@@ -23,7 +25,7 @@ INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "
                "warps_per_cam")
 PV_INFO_COUNT = 16
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
- PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE) = range(7)
+ PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, PV_OPT_GATHER_ASYNC, PV_OPT_CAM_PIPE) = range(9)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
 _P = ctypes.c_void_p

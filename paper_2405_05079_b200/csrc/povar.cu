@@ -19,6 +19,7 @@
 #include "../../include/povar.h"
 #include "pv_kernels.cuh"
 #include "pv_pcg.cuh"
+#include "pv_pipe.cuh"
 
 using namespace pv;
 
@@ -79,6 +80,11 @@ struct pv_ctx {
   bool lm_lin_fresh = false;
   int num_sms = 148;
   int wpc = 1;  // warps per camera in the camera kernels (from the mean segment size)
+  // work lists of the persistent camera kernel (k_cam_pipe)
+  int pipe_W = 0;
+  int4* d_items = nullptr;
+  int* d_item_off = nullptr;
+  size_t items_bytes = 0, item_off_bytes = 0;
   int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
@@ -95,7 +101,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1};
+  Tune tune{0, 1, 2, 2, 1, 0, 0};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -268,6 +274,84 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
 // Landmark blocks of the L2-blocked term: contiguous task ranges with ~equal
 // observation counts, sized so one block's partials s (32 B/obs) fit in the
 // budget; per camera, the camera-sorted sub-range of each block.
+template <class T>
+static void free_tracked(pv_ctx* c, T*& p, size_t bytes) {
+  if (!p) return;
+  CK(cudaFree(p));
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), (void*)p);
+  if (it != c->allocs.end()) c->allocs.erase(it);
+  c->device_bytes -= bytes;
+  p = nullptr;
+}
+
+// Work lists of k_cam_pipe (pv_pipe.cuh): for every landmark block and both passes,
+// split the cameras into pipe_W contiguous ranges of equal cost (observations + a
+// per-item overhead) and cut each (camera, block) segment into items of <= PCH
+// observations.  The W t list has >= 1 item per camera so that y is always written.
+static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
+  if (!c->pipe_W) {
+    int occ = 1 << 30;
+    auto occ_of = [&](const void* fn) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PIPE_SMEM));
+      int o = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, PW * 32, PIPE_SMEM));
+      occ = std::min(occ, o);
+    };
+    occ_of((const void*)k_cam_pipe<1, true, true>);
+    occ_of((const void*)k_cam_pipe<2, true, true>);
+    occ_of((const void*)k_cam_pipe<1, false, true>);
+    occ_of((const void*)k_cam_pipe<2, false, true>);
+    occ_of((const void*)k_cam_pipe<1, true, false>);
+    occ_of((const void*)k_cam_pipe<2, true, false>);
+    c->pipe_W = std::max(1, occ) * c->num_sms * PW;
+  }
+  const int B = c->n_blk, W = c->pipe_W;
+  const int64_t np = c->n_p;
+  constexpr int ITEM_COST = 24;  // observation-equivalents of one item's fixed overhead
+  std::vector<int4> items;
+  std::vector<int> off((size_t)2 * B * (W + 1), 0);
+  items.reserve((size_t)2 * ((size_t)c->n_os / PCH + (size_t)B * np + 16));
+  for (int L = 0; L < 2; ++L) {
+    for (int b = 0; b < B; ++b) {
+      const int* sb = seg.data() + (size_t)b * np;
+      auto n_items = [&](int64_t cam) {
+        const int n = sb[cam + 1] - sb[cam];
+        const int k = (n + PCH - 1) / PCH;
+        return L == 0 ? std::max(1, k) : k;
+      };
+      int64_t tot = 0;
+      for (int64_t cam = 0; cam < np; ++cam) tot += (sb[cam + 1] - sb[cam]) + ITEM_COST * n_items(cam);
+      int* ob = off.data() + (size_t)(L * B + b) * (W + 1);
+      ob[0] = (int)items.size();
+      int64_t cum = 0;
+      int w = 0;
+      for (int64_t cam = 0; cam < np; ++cam) {
+        // contiguous camera ranges: start the next warp once its cost share is reached
+        while (w < W - 1 && cum * W >= (int64_t)(w + 1) * tot) ob[++w] = (int)items.size();
+        const int o_lo = sb[cam], n = sb[cam + 1] - o_lo, k = n_items(cam);
+        for (int q = 0; q < k; ++q) {
+          const int o = o_lo + q * PCH;
+          const int cnt = std::max(0, std::min(PCH, o_lo + n - o));
+          items.push_back(make_int4((int)cam, o, cnt, (L ? PF_HA : 0) | (q == k - 1 ? PF_LAST : 0)));
+        }
+        cum += n + ITEM_COST * k;
+      }
+      while (w < W) ob[++w] = (int)items.size();
+    }
+  }
+  free_tracked(c, c->d_items, c->items_bytes);
+  free_tracked(c, c->d_item_off, c->item_off_bytes);
+  c->d_items = c->alloc<int4>(items.size());
+  c->d_item_off = c->alloc<int>(off.size());
+  c->items_bytes = std::max<size_t>(items.size(), 1) * sizeof(int4);
+  c->item_off_bytes = std::max<size_t>(off.size(), 1) * sizeof(int);
+  CK(cudaMemcpyAsync(c->d_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->d_item_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->stream));
+  c->sync();
+}
+
 static void build_blocks(pv_ctx* c) {
   const int n_os = c->n_os, n_tasks = c->n_tasks;
   const int64_t n_p = c->n_p;
@@ -310,12 +394,7 @@ static void build_blocks(pv_ctx* c) {
       cs_pos[p] = k;
     }
   }
-  if (c->d_seg) {
-    CK(cudaFree(c->d_seg));
-    auto it = std::find(c->allocs.begin(), c->allocs.end(), (void*)c->d_seg);
-    if (it != c->allocs.end()) c->allocs.erase(it);
-    c->device_bytes -= c->seg_bytes;
-  }
+  free_tracked(c, c->d_seg, c->seg_bytes);
   c->d_seg = c->alloc<int>(seg.size());
   c->seg_bytes = seg.size() * sizeof(int);
   CK(cudaMemcpyAsync(c->d_seg, seg.data(), seg.size() * sizeof(int), cudaMemcpyHostToDevice,
@@ -339,6 +418,7 @@ static void build_blocks(pv_ctx* c) {
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
+  build_pipe_items(c, seg);
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -453,21 +533,44 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   if (n_deg) *n_deg = fl[F_N_DEGEN];
 }
 
-template <int S, bool HC, int EP, bool HA>
-static void launch_cam(pv_ctx* c, const CamArgs& ca) {
+template <int S, bool HC, int EP, bool HA, bool GA>
+static void launch_cam_v(pv_ctx* c, const CamArgs& ca) {
+  constexpr int smem = GA ? CAM_SMEM_GA : CAM_SMEM;
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            CAM_SMEM));
+    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA, GA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            smem));
     attr_set = true;
   }
   CamArgs a = ca;
   a.wpc = c->wpc;
   const int cams_per_cta = 8 / c->wpc;
-  k_cam<S, HC, EP, HA><<<blocks_for(c->n_p, cams_per_cta), 256, CAM_SMEM, c->stream>>>(
+  k_cam<S, HC, EP, HA, GA><<<blocks_for(c->n_p, cams_per_cta), 256, smem, c->stream>>>(
       c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->cyr, c->cbp, c->cUi, c->cx, c->crhs,
       c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, a);
   c->launched();
+}
+
+template <int S, bool HC, bool HA>
+static void launch_cam_pipe(pv_ctx* c, const CamArgs& ca) {
+  PipeItems it{c->d_items, c->d_item_off, c->n_blk, c->pipe_W};
+  k_cam_pipe<S, HC, HA><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
+      c->g, it, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
+      ca.first_c, ca.a_lo, ca.check_stop);
+  c->launched();
+}
+
+template <int S, bool HC, int EP, bool HA>
+static void launch_cam(pv_ctx* c, const CamArgs& ca) {
+  if (EP == EP_NONE && c->tune.cam_pipe && !ca.project_y && (!HC || ca.c_hi == ca.c_lo + 1) &&
+      (!HA || ca.a_hi == ca.a_lo + 1)) {
+    launch_cam_pipe<S, HC, HA>(c, ca);
+    return;
+  }
+  if (HC && c->tune.gather_async)
+    launch_cam_v<S, HC, EP, HA, true>(c, ca);
+  else
+    launch_cam_v<S, HC, EP, HA, false>(c, ca);
 }
 
 template <int S, int MODE>
@@ -861,6 +964,12 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
         ncclCommDestroy(c->comm);
         c->comm = nullptr;
       }
+      break;
+    case PV_OPT_CAM_PIPE:
+      c->tune.cam_pipe = value ? 1 : 0;
+      break;
+    case PV_OPT_GATHER_ASYNC:
+      c->tune.gather_async = value ? 1 : 0;
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");

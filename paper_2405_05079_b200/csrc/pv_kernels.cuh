@@ -34,6 +34,8 @@ struct Tune {
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
   int discard_s;   // drop consumed s lines from L2 (no write-back)
+  int gather_async;  // k_cam: gather t into shared memory with cp.async one chunk ahead
+  int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -152,10 +154,19 @@ constexpr int CH = 64;                         // observations per staged chunk
 constexpr int CH_BUF = CH * 32 + CH * 16 + (CH + 8) * 4;  // x, m, ids (one buffer)
 constexpr int CAM_WARP_SMEM = 2 * CH_BUF;      // two buffers per warp
 constexpr int CAM_SMEM = 8 * CAM_WARP_SMEM;    // 8 warps per CTA
+// asynchronous-gather variant: each buffer also holds the gathered t of its chunk
+constexpr int CH_BUF_GA = CH_BUF + CH * 32;
+constexpr int CAM_SMEM_GA = 8 * 2 * CH_BUF_GA;
 
 __device__ __forceinline__ void cp_async16w(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16wp(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa),
+               "l"(gmem), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -181,6 +192,40 @@ __device__ __forceinline__ void stage_chunk(unsigned char* buf, int lane, int o,
     cp_async16w(buf + CH * 48 + 16 * lane, ids + a0 + 4 * lane);
 }
 
+// the x / m streams of one chunk (ids staged separately)
+__device__ __forceinline__ void stage_xm(unsigned char* buf, int lane, int o,
+                                         const double* __restrict__ cs_x,
+                                         const double* __restrict__ cs_m) {
+  const char* gx = reinterpret_cast<const char*>(cs_x + 4 * (size_t)o);
+#pragma unroll
+  for (int q = 0; q < (CH * 32) / (16 * 32); ++q)
+    cp_async16w(buf + 16 * (lane + 32 * q), gx + 16 * (lane + 32 * q));
+  const char* gm = reinterpret_cast<const char*>(cs_m + 2 * (size_t)o);
+#pragma unroll
+  for (int q = 0; q < (CH * 16) / (16 * 32); ++q)
+    cp_async16w(buf + CH * 32 + 16 * (lane + 32 * q), gm + 16 * (lane + 32 * q));
+}
+__device__ __forceinline__ void stage_ids(unsigned char* buf, int lane, int o,
+                                          const int* __restrict__ ids) {
+  const int a0 = o & ~3;
+  if (lane < (CH + 8) / 4) cp_async16w(buf + CH * 48 + 16 * lane, ids + a0 + 4 * lane);
+}
+// t_j of every observation of the chunk at o (landmark ids already staged in buf)
+__device__ __forceinline__ void gather_t(unsigned char* buf, int lane, int o, int o_hi,
+                                         const double* __restrict__ tarr, uint64_t pol) {
+  const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o & 3);
+  unsigned char* tb = buf + CH_BUF;
+#pragma unroll
+  for (int r = 0; r < CH / 32; ++r) {
+    const int q = lane + 32 * r;
+    if (o + q < o_hi) {
+      const double* src = tarr + 4 * (size_t)si[q];
+      cp_async16wp(tb + 32 * q, src, pol);
+      cp_async16wp(tb + 32 * q + 16, src + 2, pol);
+    }
+  }
+}
+
 struct CamArgs {
   int c_lo, c_hi;   // landmark-block range of the W t half (HC)
   int first_c;      // 1: overwrite the camera accumulator y, 0: add
@@ -192,8 +237,11 @@ struct CamArgs {
   double thr;
 };
 
-template <int STAGE, bool HC, int EP, bool HA>
-__global__ void __launch_bounds__(256) k_cam(
+#ifndef PV_CAM_MINB
+#define PV_CAM_MINB 1
+#endif
+template <int STAGE, bool HC, int EP, bool HA, bool GA>
+__global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
     Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
     const double* __restrict__ tarr, double* __restrict__ sbuf, double* __restrict__ cy,
     double* __restrict__ cyr, const double* __restrict__ cbp, const double* __restrict__ cUi,
@@ -215,7 +263,8 @@ __global__ void __launch_bounds__(256) k_cam(
   const int wpc = ca.wpc;
   const int grp = warp / wpc, gr = warp % wpc;
   const int cam = blockIdx.x * (8 / wpc) + grp;
-  unsigned char* wsm = cam_dsm + (size_t)warp * CAM_WARP_SMEM;
+  constexpr int SLOT = GA ? CH_BUF_GA : CH_BUF;
+  unsigned char* wsm = cam_dsm + (size_t)warp * 2 * SLOT;
   const bool valid = cam < g.n_p;
   const bool leader = valid && gr == 0;
   const int np = g.n_p;
@@ -238,25 +287,55 @@ __global__ void __launch_bounds__(256) k_cam(
       const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
       const int nch_all = (o_hi - o_lo + CH - 1) / CH;
       const int nch = nch_all > gr ? (nch_all - gr + wpc - 1) / wpc : 0;  // this warp's chunks
-      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
-      cp_commit();
-      for (int c = 0; c < nch; ++c) {
-        unsigned char* buf = wsm + (c & 1) * CH_BUF;
-        if (c + 1 < nch)
-          stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
-                      g.cs_m, g.cs_lm);
+      if (GA) {
+        // ids run two chunks ahead, x / m / gathered t one chunk ahead (all cp.async):
+        // chunk c computes while the t gathers of chunk c + 1 are in flight
+        if (nch > 0) {
+          stage_ids(wsm, lane, o_lo + gr * CH, g.cs_lm);
+          cp_commit();
+          cp_wait<0>();
+          __syncwarp();
+          stage_xm(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m);
+          gather_t(wsm, lane, o_lo + gr * CH, o_hi, tarr, pt);
+          if (nch > 1) stage_ids(wsm + SLOT, lane, o_lo + (gr + wpc) * CH, g.cs_lm);
+          cp_commit();
+        }
+      } else {
+        if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
         cp_commit();
-        cp_wait<1>();
-        __syncwarp();
+      }
+      for (int c = 0; c < nch; ++c) {
+        unsigned char* buf = wsm + (c & 1) * SLOT;
+        if (GA) {
+          cp_wait<0>();
+          __syncwarp();
+          if (c + 1 < nch) {
+            unsigned char* nb = wsm + ((c + 1) & 1) * SLOT;
+            const int on = o_lo + (gr + (c + 1) * wpc) * CH;
+            stage_xm(nb, lane, on, cs_x, g.cs_m);
+            gather_t(nb, lane, on, o_hi, tarr, pt);
+            if (c + 2 < nch) stage_ids(buf, lane, o_lo + (gr + (c + 2) * wpc) * CH, g.cs_lm);
+          }
+          cp_commit();
+        } else {
+          if (c + 1 < nch)
+            stage_chunk(wsm + ((c + 1) & 1) * SLOT, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
+                        g.cs_m, g.cs_lm);
+          cp_commit();
+          cp_wait<1>();
+          __syncwarp();
+        }
         const int o0 = o_lo + (gr + c * wpc) * CH;
         const double4* sx = reinterpret_cast<const double4*>(buf);
         const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
         const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
         double4 T[CH / 32];
+        if (!GA) {
 #pragma unroll
-        for (int r = 0; r < CH / 32; ++r) {
-          const int q = lane + 32 * r;
-          if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
+          for (int r = 0; r < CH / 32; ++r) {
+            const int q = lane + 32 * r;
+            if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
+          }
         }
 #pragma unroll
         for (int r = 0; r < CH / 32; ++r) {
@@ -264,9 +343,10 @@ __global__ void __launch_bounds__(256) k_cam(
           if (o0 + q < o_hi) {
             const double4 X = sx[q];
             const double2 m = sm[q];
+            const double4 Tq = GA ? reinterpret_cast<const double4*>(buf + CH_BUF)[q] : T[r];
             const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
             double sg[3];
-            proj_map<STAGE>(pj, dot4(P0, T[r]), dot4(P1, T[r]), dot4(P2v, T[r]), sg[0], sg[1],
+            proj_map<STAGE>(pj, dot4(P0, Tq), dot4(P1, Tq), dot4(P2v, Tq), sg[0], sg[1],
                             sg[2]);
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {
@@ -383,9 +463,9 @@ __global__ void __launch_bounds__(256) k_cam(
       if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_pos);
       cp_commit();
       for (int c = 0; c < nch; ++c) {
-        unsigned char* buf = wsm + (c & 1) * CH_BUF;
+        unsigned char* buf = wsm + (c & 1) * SLOT;
         if (c + 1 < nch)
-          stage_chunk(wsm + ((c + 1) & 1) * CH_BUF, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
+          stage_chunk(wsm + ((c + 1) & 1) * SLOT, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
                       g.cs_m, g.cs_pos);
         cp_commit();
         cp_wait<1>();
