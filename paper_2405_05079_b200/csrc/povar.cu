@@ -73,6 +73,12 @@ struct pv_ctx {
   // host copies kept for re-blocking (pv_set_option PV_OPT_BLOCK_BYTES)
   std::vector<int> h_ls_cam, h_ls_lid, h_task_desc;
   std::vector<int> blk_task;  // [n_blk+1] task boundaries of the landmark blocks
+  std::vector<int> blk_obs;   // [n_blk+1] landmark-sorted observation boundaries of the blocks
+  std::vector<int> h_lm_off;  // [n_ls+1]
+  // landmark-reduce work (k_lm_reduce): per block, landmarks bucketed by track length
+  std::vector<int> blk_ktask;  // [n_blk+1] warp slots
+  int4* d_klist = nullptr;
+  size_t klist_bytes = 0;
   int n_blk = 1;
   int64_t block_bytes = 80ll << 20;
   size_t seg_bytes = 0;
@@ -101,7 +107,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 0};
+  Tune tune{0, 1, 2, 2, 1, 0, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -256,6 +262,7 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->h_ls_cam = std::move(ls_cam);
   c->h_ls_lid = std::move(ls_lid);
   c->h_task_desc = task_desc;
+  c->h_lm_off = lm_off;
 
   Graph& g = c->g;
   g.n_p = (int)n_p;
@@ -352,6 +359,56 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
   c->sync();
 }
 
+// Work of the landmark reduce (k_lm_reduce, pv_kernels.cuh): per landmark block, the
+// landmarks bucketed by track length k, laid out as 32-entry warp slots of
+// {landmark, first observation, k} (one dependent load per lane).  A short slot holds up
+// to 32 landmarks of equal k <= 32 (one lane each, a k-step serial sum; unused lanes
+// have landmark -1); a long landmark (k > 32) fills a slot alone (one warp).  Longest
+// first, so the grid's tail is made of short slots.
+static void build_ktasks(pv_ctx* c) {
+  const int B = c->n_blk;
+  const std::vector<int>& off = c->h_lm_off;
+  std::vector<int4> kl;
+  kl.reserve((size_t)c->n_ls + 64 * (size_t)B);
+  c->blk_ktask.assign(B + 1, 0);
+  std::vector<std::vector<int>> bucket(33);
+  auto slot = [&](const int* ls, int n, int k) {
+    for (int q = 0; q < 32; ++q)
+      kl.push_back(q < n ? make_int4(ls[q], off[ls[q]], k, 0) : make_int4(-1, 0, k, 0));
+  };
+  for (int b = 0; b < B; ++b) {
+    const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
+    const int l0 = t0 < c->n_tasks ? c->h_task_desc[4 * t0 + 2] : c->n_ls;
+    const int l1 = t1 < c->n_tasks ? c->h_task_desc[4 * t1 + 2] : c->n_ls;
+    std::vector<std::pair<int, int>> longs;  // (k, landmark)
+    for (auto& v : bucket) v.clear();
+    for (int l = l0; l < l1; ++l) {
+      const int k = off[l + 1] - off[l];
+      if (k > 32)
+        longs.emplace_back(k, l);
+      else
+        bucket[k].push_back(l);
+    }
+    std::stable_sort(longs.begin(), longs.end(),
+                     [](const std::pair<int, int>& a, const std::pair<int, int>& x) {
+                       return a.first > x.first;
+                     });
+    for (auto& kvl : longs) slot(&kvl.second, 1, kvl.first);
+    for (int k = 32; k >= 0; --k) {
+      const std::vector<int>& v = bucket[k];
+      for (size_t i = 0; i < v.size(); i += 32)
+        slot(v.data() + i, (int)std::min<size_t>(32, v.size() - i), k);
+    }
+    c->blk_ktask[b + 1] = (int)(kl.size() / 32);
+  }
+  free_tracked(c, c->d_klist, c->klist_bytes);
+  c->d_klist = c->alloc<int4>(kl.size());
+  c->klist_bytes = std::max<size_t>(kl.size(), 1) * sizeof(int4);
+  CK(cudaMemcpyAsync(c->d_klist, kl.data(), kl.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                     c->stream));
+  c->sync();
+}
+
 static void build_blocks(pv_ctx* c) {
   const int n_os = c->n_os, n_tasks = c->n_tasks;
   const int64_t n_p = c->n_p;
@@ -418,7 +475,10 @@ static void build_blocks(pv_ctx* c) {
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
+  c->blk_obs.assign(B + 1, 0);
+  for (int b = 0; b < B; ++b) c->blk_obs[b + 1] = obs_blk_end[b];
   build_pipe_items(c, seg);
+  build_ktasks(c);
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -556,14 +616,27 @@ static void launch_cam_pipe(pv_ctx* c, const CamArgs& ca) {
   PipeItems it{c->d_items, c->d_item_off, c->n_blk, c->pipe_W};
   k_cam_pipe<S, HC, HA><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
       c->g, it, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
-      ca.first_c, ca.a_lo, ca.check_stop);
+      ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi);
   c->launched();
 }
 
+// ca.disc_lo = landmark block whose partials s were consumed by the preceding landmark
+// reduce (dropped from L2 at the start of this kernel), -1 for none
 template <int S, bool HC, int EP, bool HA>
-static void launch_cam(pv_ctx* c, const CamArgs& ca) {
-  if (EP == EP_NONE && c->tune.cam_pipe && !ca.project_y && (!HC || ca.c_hi == ca.c_lo + 1) &&
-      (!HA || ca.a_hi == ca.a_lo + 1)) {
+static void launch_cam(pv_ctx* c, const CamArgs& ca0) {
+  CamArgs ca = ca0;
+  const int db = ca.disc_lo;
+  ca.disc_lo = ca.disc_hi = 0;
+  // never drop lines this kernel itself writes (its W^T v pass scatters into blocks [a_lo, a_hi))
+  const bool writes_db = HA && db >= ca.a_lo && db < ca.a_hi;
+  if (db >= 0 && db < c->n_blk && c->tune.discard_s && !writes_db) {
+    ca.disc_lo = c->blk_obs[db];
+    ca.disc_hi = c->blk_obs[db + 1];
+  }
+  // the persistent kernel runs one warp per camera: with wpc == 1 it reproduces k_cam's
+  // summation order bit for bit, so every path (fused, sharded, blocked) stays consistent
+  if (EP == EP_NONE && c->tune.cam_pipe && c->wpc == 1 && !ca.project_y &&
+      (!HC || ca.c_hi == ca.c_lo + 1) && (!HA || ca.a_hi == ca.a_lo + 1)) {
     launch_cam_pipe<S, HC, HA>(c, ca);
     return;
   }
@@ -573,12 +646,15 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca) {
     launch_cam_v<S, HC, EP, HA, false>(c, ca);
 }
 
+// landmark half of a term over the landmark blocks [b_lo, b_hi)
 template <int S, int MODE>
-static void launch_lm_reduce(pv_ctx* c, int t_lo, int t_hi, int check_stop) {
-  const int nb = blocks_for((long long)(t_hi - t_lo) * 32, 256);  // one task per warp
-  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->g, c->sbuf, c->lrec, c->tarr, c->lsys,
-                                                  c->lbl, c->ldl, c->tlm, c->ctl, c->flags,
-                                                  c->tune, t_lo, t_hi, check_stop);
+static void launch_lm_reduce(pv_ctx* c, int b_lo, int b_hi, int check_stop) {
+  const int k_lo = c->blk_ktask[b_lo], k_hi = c->blk_ktask[b_hi];
+  const int nb = blocks_for((long long)(k_hi - k_lo) * 32, 256);  // one task per warp
+  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->d_klist, c->sbuf, c->lrec,
+                                                  c->tarr, c->lsys, c->lbl, c->ldl, c->tlm,
+                                                  c->ctl, c->flags, c->tune, k_lo, k_hi,
+                                                  check_stop);
   c->launched();
 }
 
@@ -595,6 +671,9 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
   a.project_y = 0;
   a.wpc = 1;
   a.thr = thr;
+  // a W t pass over one block follows that block's landmark reduce: its s is consumed
+  a.disc_lo = c_hi == c_lo + 1 ? c_lo : -1;
+  a.disc_hi = 0;
   return a;
 }
 
@@ -617,7 +696,7 @@ template <int S>
 static void launch_term(pv_ctx* c, int i, double thr) {
   const int B = c->n_blk;
   for (int b = 0; b < B; ++b) {
-    launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 1);
+    launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
     if (b + 1 < B)
       launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, i, thr, 1));
     else
@@ -634,7 +713,7 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   // K4: t = V+ b_l for all landmarks, then y = W t over all blocks, the reduced RHS,
   // t_0 = U^-1 rhs and the gather of block 0 (a single pass; blocking does not pay here)
   const int B = c->n_blk;
-  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_tasks, 0);
+  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
   launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, thr, 0);
   c->check_launch();
   // K5 + K6 terms with a one-term lookahead on the device stop flag
@@ -651,8 +730,10 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
   c->launched();
   for (int b = 0; b < B; ++b) {
-    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, b, b + 1, 0, thr, 0));
-    launch_lm_reduce<S, LR_BACKSUB>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+    CamArgs a = cam_args(0, 0, 0, b, b + 1, 0, thr, 0);
+    a.disc_lo = b - 1;  // consumed by the previous block's back-substitution
+    launch_cam<S, false, EP_NONE, true>(c, a);
+    launch_lm_reduce<S, LR_BACKSUB>(c, b, b + 1, 0);
   }
   c->check_launch();
   PowerCtl h;
@@ -681,7 +762,7 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   const int wg = blocks_for((long long)np * 32, 256);  // one warp per camera
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_M, 0, 2 * sizeof(int), c->stream));
   // K4: the reduced RHS (its U^-1 epilogue output is unused here)
-  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_tasks, 0);
+  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
   launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, 0.0, 0);
   // preconditioner: exact block diagonal and its inverse (solvers.py:161-166)
   k_schur_diag<S><<<wg, 256, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->lsys, c->cmom, c->coef);
@@ -716,7 +797,7 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   for (int it = 1; it <= max_it && !((volatile PowerCtl*)c->host_ctl)->stopped; ++it) {
     launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 1));
     for (int b = 0; b < B; ++b) {
-      launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 1);
+      launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
       if (b + 1 < B)
         launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, 0, 0.0, 1));
       else
@@ -740,8 +821,10 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   k_setv<S><<<blocks_for(np, 128), 128, 0, c->stream>>>((int)np, c->cx, c->ch, c->crec);
   c->launched();
   for (int b = 0; b < B; ++b) {
-    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0));
-    launch_lm_reduce<S, LR_BACKSUB>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+    CamArgs a = cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0);
+    a.disc_lo = b - 1;
+    launch_cam<S, false, EP_NONE, true>(c, a);
+    launch_lm_reduce<S, LR_BACKSUB>(c, b, b + 1, 0);
   }
   c->check_launch();
   PowerCtl h;
@@ -1166,7 +1249,7 @@ static void op_schur_apply(pv_ctx* c, const double* v, double* out) {
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->ctmp, c->ch, c->crec);
   c->launched();
   launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, c->n_blk, 0, 0.0, 0));
-  launch_lm_reduce<S, LR_TERM>(c, 0, c->n_tasks, 0);
+  launch_lm_reduce<S, LR_TERM>(c, 0, c->n_blk, 0);
   launch_cam<S, true, EP_NONE, false>(c, cam_args(0, c->n_blk, 1, 0, 0, 0, 0.0, 0));
   c->allreduce(c->cy, (size_t)c->n_p * 12);
   k_project_y<S><<<blocks_for(c->n_p * 32, 256), 256, 0, c->stream>>>((int)c->n_p, c->cy, c->ch,
@@ -1202,7 +1285,7 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   for (int i = 1; i <= n; ++i) {
     // whole term timed end to end; per-kernel split measured on the first block
     CK(cudaEventRecord(c->tev[0], c->stream));
-    launch_lm_reduce<S, LR_TERM>(c, c->blk_task[0], c->blk_task[1], 0);
+    launch_lm_reduce<S, LR_TERM>(c, 0, 1, 0);
     CK(cudaEventRecord(c->tev[1], c->stream));
     const int B = c->n_blk;
     if (B > 1)
@@ -1211,7 +1294,7 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
       launch_cam_last<S, EP_TERM>(c, 0, 1, 1, 1 << 20, -1.0, 0);
     CK(cudaEventRecord(c->tev[2], c->stream));
     for (int b = 1; b < B; ++b) {
-      launch_lm_reduce<S, LR_TERM>(c, c->blk_task[b], c->blk_task[b + 1], 0);
+      launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 0);
       if (b + 1 < B)
         launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, 0, b + 1, b + 2, 1 << 20, -1.0,
                                                        0));

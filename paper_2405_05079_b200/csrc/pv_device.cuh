@@ -66,9 +66,16 @@ __device__ __forceinline__ uint64_t pol_normal() {
   asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// 0 normal, 1 evict_first, 2 evict_last
+// 0 normal, 1 evict_first, 2 evict_last (one createpolicy per call: `which` is uniform)
 __device__ __forceinline__ uint64_t pol_sel(int which) {
-  return which == 1 ? pol_first() : (which == 2 ? pol_last() : pol_normal());
+  uint64_t p;
+  if (which == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (which == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ double4 ldg4p(const double* p, uint64_t pol) {
   double4 v;

@@ -129,6 +129,17 @@ __device__ __forceinline__ int seg_start_lane(const Task& t, int lane) {
 // Both transpositions of S'.v therefore stay on chip; DRAM only streams the
 // camera-sorted observation data (x, m, ids) twice per term.
 
+// the consumed partials of a landmark block are scratch: drop their L2 lines instead of
+// writing them back (lines entirely inside [o_lo, o_hi) only); grid-stride, all threads
+__device__ __forceinline__ void discard_s_lines(double* sbuf, int o_lo, int o_hi) {
+  if (o_hi <= o_lo) return;
+  const size_t l0 = (32ull * o_lo + 127) / 128, l1 = (32ull * o_hi) / 128;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t ln = l0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; ln < l1; ln += stride)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(sbuf) + ln * 128)
+                 : "memory");
+}
+
 enum { EP_NONE = 0, EP_RHS = 1, EP_TERM = 2 };
 
 __device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT/32*12]*/,
@@ -234,6 +245,7 @@ struct CamArgs {
   int check_stop;   // return immediately once the series has stopped
   int project_y;    // write the (stage-2 projected) y to cyr instead (schur apply)
   int wpc;          // warps per camera (1, 2, 4, 8)
+  int disc_lo, disc_hi;  // landmark-sorted observations whose consumed partials s are dropped
   double thr;
 };
 
@@ -258,6 +270,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
   __shared__ double gv[8][12];
   extern __shared__ __align__(32) unsigned char cam_dsm[];
   if (ca.check_stop && ctl->stopped) return;  // grid-uniform
+  discard_s_lines(sbuf, ca.disc_lo, ca.disc_hi);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpc = ca.wpc;
@@ -334,7 +347,11 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
 #pragma unroll
           for (int r = 0; r < CH / 32; ++r) {
             const int q = lane + 32 * r;
+#ifdef PV_EXP_SEQ_GATHER  // timing experiment only: wrong results
+            if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)((o0 + q) % g.n_l), pt);
+#else
             if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
+#endif
           }
         }
 #pragma unroll
@@ -489,7 +506,11 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
             sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
             sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
             sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
+#ifdef PV_EXP_SEQ_SCATTER  // timing experiment only: wrong results
+            st4p(sbuf + 4 * (size_t)(o0 + q) + 0 * pos, sv, ps);
+#else
             st4p(sbuf + 4 * (size_t)pos, sv, ps);
+#endif
           }
         }
         __syncwarp();
@@ -657,11 +678,45 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
   }
 }
 
-// One landmark task per warp.  Lean on instructions (the kernel is issue-bound): only
-// the live components are reduced (3 in stage 1), the shuffle tree stops at the
-// task's longest segment, the heads' V+ loads are issued before the reduction.
+// Landmark half of a term.  Work unit (built by build_ktasks, povar.cu): up to 32
+// landmarks of one block with the same track length k <= 32, one lane per landmark,
+// each lane summing its k partials s_ij serially (k is warp-uniform: no divergence,
+// no shuffles, ~5 instructions per observation); a landmark with k > 32 is a unit of
+// its own, reduced by the whole warp (coalesced, fixed-order tree).  Deterministic.
+
 template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__ sbuf,
+__device__ __forceinline__ void lr_long(const Task& t, int lane, const double* __restrict__ sbuf,
+                                        const double* __restrict__ lrec,
+                                        double* __restrict__ tarr,
+                                        const double* __restrict__ lsys,
+                                        const double* __restrict__ lbl, double* __restrict__ ldl,
+                                        double* __restrict__ tlm, int* flags, uint64_t pf,
+                                        uint64_t pt) {
+  constexpr int NV = STAGE == 1 ? 3 : 4;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const LmPre pre = lane == 0 ? lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl) : LmPre{};
+  if (MODE != LR_RHS) {
+    double a2[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a2[i] = 0.0;
+#pragma unroll 4
+    for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
+      const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
+      a2[0] += s.x;
+      a2[1] += s.y;
+      a2[2] += s.z;
+      if (NV == 4) a2[NV - 1] += s.w;
+    }
+    warp_reduce_all(a2);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = a2[i];
+  }
+  if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
+}
+
+template <int STAGE, int MODE>
+__global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klist,
+                                                   const double* __restrict__ sbuf,
                                                    const double* __restrict__ lrec,
                                                    double* __restrict__ tarr,
                                                    const double* __restrict__ lsys,
@@ -669,74 +724,40 @@ __global__ void __launch_bounds__(256) k_lm_reduce(Graph g, double* __restrict__
                                                    double* __restrict__ ldl,
                                                    double* __restrict__ tlm,
                                                    const PowerCtl* __restrict__ ctl, int* flags,
-                                                   Tune tune, int task_lo, int task_hi,
+                                                   Tune tune, int k_lo, int k_hi,
                                                    int check_stop) {
-  constexpr int NV = STAGE == 1 ? 3 : 4;
   const int lane = threadIdx.x & 31;
-  const int w = task_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (w >= task_hi) return;
+  const int w = k_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (w >= k_hi) return;
   if (check_stop && ctl->stopped) return;
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
-  const Task t = load_task(g, w, lane);
+  const int4 e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k}
+  const int k = e.z;                                      // warp-uniform
+  if (k > 32) {
+    Task t;
+    t.l0 = __shfl_sync(PV_FULL, e.x, 0);
+    t.o0 = __shfl_sync(PV_FULL, e.y, 0);
+    t.n = k;
+    t.long_task = true;
+    t.heads = 1u;
+    lr_long<STAGE, MODE>(t, lane, sbuf, lrec, tarr, lsys, lbl, ldl, tlm, flags, pf, pt);
+    return;
+  }
+  if (e.x < 0) return;
+  const LmPre pre = lm_prefetch<STAGE, MODE>(e.x, lrec, lsys, lbl);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (t.long_task) {
-    const LmPre pre = lane == 0 ? lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl) : LmPre{};
-    if (MODE != LR_RHS) {
-      double a2[NV];
-#pragma unroll
-      for (int i = 0; i < NV; ++i) a2[i] = 0.0;
+  if (MODE != LR_RHS) {
+    const double* sp = sbuf + 4 * (size_t)e.y;
 #pragma unroll 4
-      for (int o = t.o0 + lane; o < t.o0 + t.n; o += 32) {
-        const double4 s = ldg4p(sbuf + 4 * (size_t)o, pf);
-        a2[0] += s.x;
-        a2[1] += s.y;
-        a2[2] += s.z;
-        if (NV == 4) a2[NV - 1] += s.w;
-      }
-      warp_reduce_all(a2);
-#pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = a2[i];
+    for (int i = 0; i < k; ++i) {
+      const double4 v = ldg4p(sp + 4 * i, pf);
+      acc[0] += v.x;
+      acc[1] += v.y;
+      acc[2] += v.z;
+      if (STAGE == 2) acc[3] += v.w;
     }
-    if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
-  } else {
-    int l, seg_end;
-    lane_segment(t, lane, l, seg_end);
-    const bool head = lane < t.n && ((t.heads >> lane) & 1u);
-    double a2[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) a2[i] = 0.0;
-    if (MODE != LR_RHS && lane < t.n) {
-      const double4 s = ldg4p(sbuf + 4 * (size_t)(t.o0 + lane), pf);
-      a2[0] = s.x;
-      a2[1] = s.y;
-      a2[2] = s.z;
-      if (NV == 4) a2[NV - 1] = s.w;
-    }
-    LmPre pre;
-    if (head) pre = lm_prefetch<STAGE, MODE>(l, lrec, lsys, lbl);
-    if (MODE != LR_RHS) {
-      const unsigned len = head ? (unsigned)(seg_end - lane) : 1u;
-      const int max_len = (int)__reduce_max_sync(PV_FULL, len);
-      seg_reduce_n(a2, lane, seg_end, max_len);
-    }
-#pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = a2[i];
-    if (head) lm_finish<STAGE, MODE>(l, acc, pre, tarr, ldl, tlm, flags, pt);
   }
-  if (MODE == LR_TERM && tune.discard_s) {
-    // the consumed partials are scratch: drop their L2 lines instead of writing them back
-    // (only lines entirely inside this task's observation range)
-    const unsigned l0 = (unsigned)((4ull * t.o0 * sizeof(double) + 127) / 128);
-    const unsigned l1 = (unsigned)((4ull * (t.o0 + t.n) * sizeof(double)) / 128);
-    if (l0 + lane < l1)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(sbuf) +
-                                                       (size_t)(l0 + lane) * 128)
-                   : "memory");
-    for (unsigned ln = l0 + 32 + lane; ln < l1; ln += 32)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(sbuf) +
-                                                       (size_t)ln * 128)
-                   : "memory");
-  }
+  lm_finish<STAGE, MODE>(e.x, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
 // block-major camera-sorted copy of the measurements (once per re-blocking)

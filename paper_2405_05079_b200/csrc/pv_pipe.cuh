@@ -29,10 +29,10 @@ namespace pv {
 #define PV_PIPE_CH 64
 #endif
 #ifndef PV_PIPE_D
-#define PV_PIPE_D 4
+#define PV_PIPE_D 3
 #endif
 #ifndef PV_PIPE_W
-#define PV_PIPE_W 4
+#define PV_PIPE_W 2
 #endif
 #ifndef PV_PIPE_MINB
 #define PV_PIPE_MINB 1
@@ -117,9 +117,10 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
                                                       double* __restrict__ cy,
                                                       const PowerCtl* __restrict__ ctl, Coef k,
                                                       Tune tune, int bc, int first_c, int ba,
-                                                      int check_stop) {
+                                                      int check_stop, int disc_lo, int disc_hi) {
   extern __shared__ __align__(128) unsigned char pipe_dsm[];
   if (check_stop && ctl->stopped) return;  // grid-uniform
+  discard_s_lines(sbuf, disc_lo, disc_hi);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * PW + warp;
@@ -195,7 +196,10 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     if (h.w & PF_HA) return;
     const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (h.y & 3);
     unsigned char* tb = tbuf + (item & 1) * PT_BYTES;
-    for (int q = lane; q < h.z; q += 32) {
+#pragma unroll
+    for (int r = 0; r < PCH / 32; ++r) {
+      const int q = lane + 32 * r;
+      if (q >= h.z) continue;
       const double* src = tarr + 4 * (size_t)si[q];
       cp_async16wp(tb + 32 * q, src, pt);
       cp_async16wp(tb + 32 * q + 16, src + 2, pt);
@@ -236,7 +240,10 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
         if (n > 0) {
           const double4 P0 = cr[0], P1 = cr[1], P2v = cr[2];
           const double4* tq = reinterpret_cast<const double4*>(tbuf + (c & 1) * PT_BYTES);
-          for (int q = lane; q < n; q += 32) {
+#pragma unroll
+          for (int r = 0; r < PCH / 32; ++r) {
+            const int q = lane + 32 * r;
+            if (q >= n) continue;
             const double4 X = sx[q];
             const double2 m = sm[q];
             const double4 T = tq[q];
@@ -270,7 +277,10 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
       const double4 P0 = cr[0], P1 = cr[1], P2v = cr[2];
       const double4 v0 = cr[3], v1 = cr[4], v2 = cr[5];
       const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (o0 & 3);
-      for (int q = lane; q < n; q += 32) {
+#pragma unroll
+      for (int r = 0; r < PCH / 32; ++r) {
+        const int q = lane + 32 * r;
+        if (q >= n) continue;
         const double4 X = sx[q];
         const double2 m = sm[q];
         const int pos = si[q];
