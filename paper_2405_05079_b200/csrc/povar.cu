@@ -372,9 +372,12 @@ static void build_ktasks(pv_ctx* c) {
   kl.reserve((size_t)c->n_ls + 64 * (size_t)B);
   c->blk_ktask.assign(B + 1, 0);
   std::vector<std::vector<int>> bucket(33);
+  constexpr int SL = 32 / LG;  // landmarks per short slot (each entry repeated LG times)
   auto slot = [&](const int* ls, int n, int k) {
-    for (int q = 0; q < 32; ++q)
-      kl.push_back(q < n ? make_int4(ls[q], off[ls[q]], k, 0) : make_int4(-1, 0, k, 0));
+    for (int q = 0; q < 32; ++q) {
+      const int i = q / LG;
+      kl.push_back(i < n ? make_int4(ls[i], off[ls[i]], k, 0) : make_int4(-1, 0, k, 0));
+    }
   };
   for (int b = 0; b < B; ++b) {
     const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
@@ -393,11 +396,14 @@ static void build_ktasks(pv_ctx* c) {
                      [](const std::pair<int, int>& a, const std::pair<int, int>& x) {
                        return a.first > x.first;
                      });
-    for (auto& kvl : longs) slot(&kvl.second, 1, kvl.first);
+    for (auto& kvl : longs) {  // a long landmark fills a slot alone: entry 0, rest empty
+      kl.push_back(make_int4(kvl.second, off[kvl.second], kvl.first, 0));
+      for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, kvl.first, 0));
+    }
     for (int k = 32; k >= 0; --k) {
       const std::vector<int>& v = bucket[k];
-      for (size_t i = 0; i < v.size(); i += 32)
-        slot(v.data() + i, (int)std::min<size_t>(32, v.size() - i), k);
+      for (size_t i = 0; i < v.size(); i += SL)
+        slot(v.data() + i, (int)std::min<size_t>(SL, v.size() - i), k);
     }
     c->blk_ktask[b + 1] = (int)(kl.size() / 32);
   }

@@ -714,6 +714,11 @@ __device__ __forceinline__ void lr_long(const Task& t, int lane, const double* _
   if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
+#ifndef PV_LR_G
+#define PV_LR_G 1
+#endif
+constexpr int LG = PV_LR_G;  // lanes per landmark in a short warp slot (1, 2, 4, 8)
+
 template <int STAGE, int MODE>
 __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klist,
                                                    const double* __restrict__ sbuf,
@@ -743,21 +748,32 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
     lr_long<STAGE, MODE>(t, lane, sbuf, lrec, tarr, lsys, lbl, ldl, tlm, flags, pf, pt);
     return;
   }
-  if (e.x < 0) return;
-  const LmPre pre = lm_prefetch<STAGE, MODE>(e.x, lrec, lsys, lbl);
+  // LG lanes per landmark (the slot entry is repeated LG times): lane j of a group sums
+  // the observations i = j, j + LG, ... (adjacent lanes read adjacent sectors), then a
+  // fixed xor tree inside the group; the group's first lane finishes the landmark
+  if (e.x < 0) return;  // whole groups are empty together
+  const int j = lane & (LG - 1);
+  LmPre pre;
+  if (j == 0) pre = lm_prefetch<STAGE, MODE>(e.x, lrec, lsys, lbl);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (MODE != LR_RHS) {
     const double* sp = sbuf + 4 * (size_t)e.y;
 #pragma unroll 4
-    for (int i = 0; i < k; ++i) {
+    for (int i = j; i < k; i += LG) {
       const double4 v = ldg4p(sp + 4 * i, pf);
       acc[0] += v.x;
       acc[1] += v.y;
       acc[2] += v.z;
       if (STAGE == 2) acc[3] += v.w;
     }
+#pragma unroll
+    for (int d = 1; d < LG; d <<= 1) {
+      const unsigned gm = __activemask();
+#pragma unroll
+      for (int c = 0; c < (STAGE == 1 ? 3 : 4); ++c) acc[c] += __shfl_xor_sync(gm, acc[c], d);
+    }
   }
-  lm_finish<STAGE, MODE>(e.x, acc, pre, tarr, ldl, tlm, flags, pt);
+  if (j == 0) lm_finish<STAGE, MODE>(e.x, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
 // block-major camera-sorted copy of the measurements (once per re-blocking)
