@@ -557,7 +557,13 @@ static int op_linearize(pv_ctx* c) {
     c->launched();
   }
   c->lm_lin_fresh = false;
-  k_lin_cam<S><<<(int)c->n_p, FT, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->cUraw, c->coef);
+  static bool lin_attr = false;
+  if (!lin_attr) {
+    CK(cudaFuncSetAttribute(k_lin_cam<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, LIN_SMEM));
+    lin_attr = true;
+  }
+  k_lin_cam<S><<<(int)c->n_p, FT, LIN_SMEM, c->stream>>>(c->g, c->crec, c->cs_x, c->cUraw,
+                                                         c->coef);
   c->launched(2);
   c->check_launch();
   c->allreduce(c->cUraw, (size_t)c->n_p * LINP);

@@ -916,6 +916,10 @@ __global__ void __launch_bounds__(256) k_lin_lm(Graph g, const double* __restric
 //            h = dpi^T r (objective.py:128-146)
 // Output: 78 upper entries of U (row-major i <= j) + 12 of b_p per camera.
 
+constexpr int LC_BUF = 3;                   // staging buffers of k_lin_cam
+constexpr int LC_BYTES = FT * 48;           // x (32 B) + m (16 B) per observation
+constexpr int LIN_SMEM = LC_BUF * LC_BYTES;
+
 template <int STAGE>
 __global__ void __launch_bounds__(FT, 2) k_lin_cam(Graph g, const double* __restrict__ crec,
                                                const double* __restrict__ cs_x,
@@ -941,65 +945,103 @@ __global__ void __launch_bounds__(FT, 2) k_lin_cam(Graph g, const double* __rest
   double acc[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.0;
-  // flattened walk over this camera's segments (one per landmark block)
-  int b = 0, o = nb > 0 ? s_lo[0] + gt : 0;
-  while (b < nb && o >= s_hi[b]) {
-    const int over = o - s_hi[b];
-    ++b;
-    if (b < nb) o = s_lo[b] + over;
-  }
-  while (b < nb) {
-    const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
-    const double4 X = ldg4(cs_x + 4 * (size_t)o);
-    double w[4], h[3];
-    const double u0 = dot4(P0, X), u1 = dot4(P1, X), u2 = dot4(P2, X);
-    if (STAGE == 1) {
-      const double r0 = k.s1 * (u0 - u2 * m.x), r1 = k.s1 * (u1 - u2 * m.y);
-      const double r2 = k.s2 * (u0 - m.x), r3 = k.s2 * (u1 - m.y);
-      w[0] = 1.0;
-      w[1] = m.x;
-      w[2] = m.y;
-      w[3] = m.x * m.x + m.y * m.y;
-      h[0] = fma(k.s1, r0, k.s2 * r2);
-      h[1] = fma(k.s1, r1, k.s2 * r3);
-      h[2] = -k.s1 * fma(m.x, r0, m.y * r1);
-    } else {
-      const double iz = 1.0 / u2, i2 = iz * iz;
-      const double p0 = u0 * iz, p1 = u1 * iz;
-      const double r0 = u0 / u2 - m.x, r1 = u1 / u2 - m.y;
-      w[0] = i2;
-      w[1] = p0 * i2;
-      w[2] = p1 * i2;
-      w[3] = (p0 * p0 + p1 * p1) * i2;
-      h[0] = iz * r0;
-      h[1] = iz * r1;
-      h[2] = -iz * fma(p0, r0, p1 * r1);
+  // The camera's observations (one segment per landmark block) are cut into chunks of
+  // <= FT observations, staged (x, m) into shared memory by cp.async two chunks ahead
+  // (LC_BUF buffers); each group's thread gt takes observations gt and gt + GT of a chunk.
+  extern __shared__ __align__(32) unsigned char lin_dsm[];
+  int wb = 0, wo = nb > 0 ? s_lo[0] : 0;  // walker: next chunk = (block wb, first obs wo)
+  auto next_chunk = [&](int& o, int& n) {  // uniform over the CTA
+    while (wb < nb && wo >= s_hi[wb]) {
+      ++wb;
+      if (wb < nb) wo = s_lo[wb];
     }
-    const double xv[4] = {X.x, X.y, X.z, X.w};
-    const double wa = grp == 0 ? w[0] : w[2], wb = grp == 0 ? w[1] : w[3];
-    int e = 0;
-#pragma unroll
-    for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-      for (int b2 = a2; b2 < 4; ++b2) {
-        const double xx = xv[a2] * xv[b2];
-        acc[e] = fma(wa, xx, acc[e]);
-        acc[10 + e] = fma(wb, xx, acc[10 + e]);
-        ++e;
+    if (wb >= nb) {
+      o = 0;
+      n = 0;
+      return;
+    }
+    o = wo;
+    n = min(FT, s_hi[wb] - wo);
+    wo += n;
+  };
+  static_assert(LC_BUF == 3, "chunk counts rotate through three registers");
+  int n0 = 0, n1 = 0, n2 = 0;  // observation counts of chunks c, c + 1, c + 2
+  auto stage = [&](int slot) {
+    int o, n;
+    next_chunk(o, n);
+    n2 = n;
+    unsigned char* buf = lin_dsm + (size_t)slot * LC_BYTES;
+    if (tid < n) {
+      const double* gx = cs_x + 4 * (size_t)(o + tid);
+      cp_async16w(buf + 32 * tid, gx);
+      cp_async16w(buf + 32 * tid + 16, gx + 2);
+      cp_async16w(buf + FT * 32 + 16 * tid, g.cs_m + 2 * (size_t)(o + tid));
+    }
+    cp_commit();
+  };
+  stage(0);
+  n0 = n2;
+  stage(1);
+  n1 = n2;
+  for (int c = 0;; ++c) {
+    const int slot = c % LC_BUF;
+    if (n0 == 0) break;  // chunks come in order: an empty one ends the list
+    stage((c + LC_BUF - 1) % LC_BUF);
+    cp_wait<LC_BUF - 1>();
+    __syncthreads();
+    const unsigned char* buf = lin_dsm + (size_t)slot * LC_BYTES;
+    for (int q = gt; q < n0; q += GT) {
+      const double2 m = reinterpret_cast<const double2*>(buf + FT * 32)[q];
+      const double4 X = reinterpret_cast<const double4*>(buf)[q];
+      double w[4], h[3];
+      const double u0 = dot4(P0, X), u1 = dot4(P1, X), u2 = dot4(P2, X);
+      if (STAGE == 1) {
+        const double r0 = k.s1 * (u0 - u2 * m.x), r1 = k.s1 * (u1 - u2 * m.y);
+        const double r2 = k.s2 * (u0 - m.x), r3 = k.s2 * (u1 - m.y);
+        w[0] = 1.0;
+        w[1] = m.x;
+        w[2] = m.y;
+        w[3] = m.x * m.x + m.y * m.y;
+        h[0] = fma(k.s1, r0, k.s2 * r2);
+        h[1] = fma(k.s1, r1, k.s2 * r3);
+        h[2] = -k.s1 * fma(m.x, r0, m.y * r1);
+      } else {
+        const double iz = 1.0 / u2, i2 = iz * iz;
+        const double p0 = u0 * iz, p1 = u1 * iz;
+        const double r0 = u0 / u2 - m.x, r1 = u1 / u2 - m.y;
+        w[0] = i2;
+        w[1] = p0 * i2;
+        w[2] = p1 * i2;
+        w[3] = (p0 * p0 + p1 * p1) * i2;
+        h[0] = iz * r0;
+        h[1] = iz * r1;
+        h[2] = -iz * fma(p0, r0, p1 * r1);
       }
-    if (grp == 1) {
+      const double xv[4] = {X.x, X.y, X.z, X.w};
+      const double wa = grp == 0 ? w[0] : w[2], wb2 = grp == 0 ? w[1] : w[3];
+      int e = 0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+      for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
-        for (int a2 = 0; a2 < 4; ++a2) acc[20 + 4 * c + a2] = fma(h[c], xv[a2], acc[20 + 4 * c + a2]);
+        for (int b2 = a2; b2 < 4; ++b2) {
+          const double xx = xv[a2] * xv[b2];
+          acc[e] = fma(wa, xx, acc[e]);
+          acc[10 + e] = fma(wb2, xx, acc[10 + e]);
+          ++e;
+        }
+      if (grp == 1) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+          for (int a2 = 0; a2 < 4; ++a2)
+            acc[20 + 4 * cc + a2] = fma(h[cc], xv[a2], acc[20 + 4 * cc + a2]);
+      }
     }
-    o += GT;
-    while (b < nb && o >= s_hi[b]) {
-      const int over = o - s_hi[b];
-      ++b;
-      if (b < nb) o = s_lo[b] + over;
-    }
+    __syncthreads();  // the buffer is refilled next iteration
+    n0 = n1;
+    n1 = n2;
   }
+  cp_wait<0>();
   // fixed-order block reduction (per group)
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1)
