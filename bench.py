@@ -114,11 +114,11 @@ def term_bytes(n_p, n_l, n_o, stage=1):
     and one id (4) twice -- once for W t, once for W^T v -- scatters s (32) and
     reads each landmark's t once (32 per landmark), plus per camera P, U^-1 and
     the small vectors (~1.6 KB).  k_lm_reduce reads s (32 per observation) and
-    per landmark the task descriptor, V+ (2 x 32 B sectors), x (stage 2) and
+    per landmark its work-slot entry (16), V+ (2 x 32 B sectors), x (stage 2) and
     writes t (32).  s and t are sized per block to stay in the persisting L2,
     so the DRAM-compulsory part is the streams + per-landmark data.
     """
-    lmr = 32 * n_o + (104 if stage == 1 else 136) * n_l
+    lmr = 32 * n_o + (112 if stage == 1 else 144) * n_l
     cam = 136 * n_o + 32 * n_l + 1600 * n_p
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
     return {"lm_reduce": lmr, "cam": cam, "r1_term": r1}
@@ -290,8 +290,10 @@ def main():
     loc = dp.info()
     tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], 1)
     kern = {}
+    # one warp per camera: the persistent TMA-pipelined camera kernel runs the blocks
+    cam_name = "k_cam_pipe" if loc["warps_per_cam"] == 1 else "k_cam"
     for name, key, tkey in (("k_lm_reduce", "lm_reduce", "phase1_ms"),
-                            ("k_cam", "cam", "phase2_ms")):
+                            (cam_name, "cam", "phase2_ms")):
         ms = kt[tkey]
         gbs = tb[key] / (ms * 1e-3) / 1e9
         kern[name] = {"ms": ms, "algorithmic_bytes": tb[key], "achieved_gbs": gbs,
