@@ -107,7 +107,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 1};
+  Tune tune{0, 1, 2, 2, 1, 0, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -140,9 +140,11 @@ struct pv_ctx {
 
   int nblk_tasks() const { return blocks_for((long long)n_tasks * 32, 256); }
   // deterministic sum of n_tasks warp partials into scal[0] (two levels)
-  void sum_partials() {
-    const int nb2 = std::max(1, std::min(256, (n_tasks + 4095) / 4096));
-    k_sum<<<nb2, 1024, 0, stream>>>(cpart, std::max(n_tasks, 1), cpart + n_tasks + 8);
+  // deterministic sum of n (default n_tasks <= the buffer's capacity) warp partials
+  void sum_partials(int n = -1) {
+    if (n < 0) n = n_tasks;
+    const int nb2 = std::max(1, std::min(256, (n + 4095) / 4096));
+    k_sum<<<nb2, 1024, 0, stream>>>(cpart, std::max(n, 1), cpart + n_tasks + 8);
     k_sum<<<1, 1024, 0, stream>>>(cpart + n_tasks + 8, nb2, scal);
     launched(2);
   }
@@ -863,10 +865,18 @@ static void op_trial(pv_ctx* c, int* ok) {
 
 static void op_resolve_trial(pv_ctx* c, double* f_new, int64_t* n_rd) {
   CK(cudaMemsetAsync(c->flags + F_N_RANKDEF, 0, 2 * sizeof(int), c->stream));
-  k_resolve<<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
-      c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef, c->lvr, c->lbl);
-  c->launched();
-  c->sum_partials();
+  if (c->tune.resolve_slots) {
+    const int ns = c->blk_ktask[c->n_blk];  // every landmark block's slots, in order
+    k_resolve_slots<<<blocks_for((long long)ns * 32, 256), 256, 0, c->stream>>>(
+        c->g, c->d_klist, ns, c->tcam, c->tlm, c->cpart, c->flags, c->coef, c->lvr, c->lbl);
+    c->launched();
+    c->sum_partials(ns);
+  } else {
+    k_resolve<<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
+        c->g, c->tcam, c->tlm, c->cpart, c->flags, c->coef, c->lvr, c->lbl);
+    c->launched();
+    c->sum_partials();
+  }
   c->check_launch();
   c->allreduce(c->scal, 1);
   c->allreduce_flags();
@@ -1059,6 +1069,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
         ncclCommDestroy(c->comm);
         c->comm = nullptr;
       }
+      break;
+    case PV_OPT_RESOLVE_SLOTS:
+      c->tune.resolve_slots = value ? 1 : 0;
       break;
     case PV_OPT_CAM_PIPE:
       c->tune.cam_pipe = value ? 1 : 0;

@@ -36,6 +36,7 @@ struct Tune {
   int discard_s;   // drop consumed s lines from L2 (no write-back)
   int gather_async;  // k_cam: gather t into shared memory with cp.async one chunk ahead
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
+  int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -1676,6 +1677,138 @@ __global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __rest
     if (bfb) atomicAdd(flags + F_N_FALLBACK, __popc(bfb));
   }
   warp_partial(cost, part);
+}
+
+// Landmark re-solve, lane-per-landmark form (the same k-bucketed warp slots as the
+// landmark reduce): each lane owns one landmark with k <= 32 observations and walks them
+// serially -- pass 1 builds [A^T A | A^T c] (no shuffles), the lane solves (every lane
+// busy), an ill-conditioned landmark repeats the walk for the CholeskyQR2 pass, and a
+// last walk evaluates the stage-1 cost at the new coordinates.  The observation rows are
+// rebuilt in each walk from the (L1/L2-resident) trial cameras instead of being shuffled.
+// A landmark with k > 32 fills a slot alone and is processed by the whole warp.
+__device__ __forceinline__ Rows4 resolve_obs(const Graph& g, const double* __restrict__ tcam,
+                                             int o, const Coef& k) {
+  const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+  return resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
+}
+
+// per-landmark solve from the pass-1 Gram (returns fb: 0 solved, 1 needs pass 2, 2 Givens)
+__device__ __forceinline__ int resolve_pass1(const double* g1, double* R1, double* v) {
+  const double ratio = chol3(g1, R1);
+  const int fb = ratio >= NE_PIVOT_TOL ? 0 : (ratio > CQR_PIVOT_TOL ? 1 : 2);
+  if (fb == 0) ne_solve(R1, g1 + 6, v);
+  return fb;
+}
+
+__device__ __forceinline__ void resolve_store(int l, const double* g1, const double* v, bool full,
+                                              double* __restrict__ tlm, double* __restrict__ lvr,
+                                              double* __restrict__ lbl, double4& x) {
+  const double4 old = ld4(tlm + (size_t)l * 4);
+  x.x = full ? v[0] : old.x;
+  x.y = full ? v[1] : old.y;
+  x.z = full ? v[2] : old.z;
+  x.w = full ? 1.0 : old.w;
+  st4(tlm + (size_t)l * 4, x);
+  if (lvr != nullptr) {
+    // the next stage-1 linearization at this state: V = A^T A (J_l does not depend on x)
+    // and b_l = J_l^T r = A^T (A x + c)
+    double* vo = lvr + (size_t)l * 8;
+    st4(vo, make_double4(g1[0], g1[1], g1[2], g1[3]));
+    st4(vo + 4, make_double4(g1[4], g1[5], 0.0, 0.0));
+    const double b0 = fma(g1[0], x.x, fma(g1[1], x.y, fma(g1[2], x.z, g1[6] * x.w)));
+    const double b1 = fma(g1[1], x.x, fma(g1[3], x.y, fma(g1[4], x.z, g1[7] * x.w)));
+    const double b2 = fma(g1[2], x.x, fma(g1[4], x.y, fma(g1[5], x.z, g1[8] * x.w)));
+    st4(lbl + (size_t)l * 4, make_double4(b0, b1, b2, 0.0));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __restrict__ klist,
+                                                       int n_slots,
+                                                       const double* __restrict__ tcam,
+                                                       double* __restrict__ tlm,
+                                                       double* __restrict__ part, int* flags,
+                                                       Coef k, double* __restrict__ lvr,
+                                                       double* __restrict__ lbl) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_slots) return;
+  const int4 e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k}
+  const int kk = e.z;                                     // warp-uniform
+  double cost = 0.0;
+  int rankdef = 0, fallback = 0;
+  if (kk > 32) {  // one long landmark: the warp strides over its observations
+    const int l = __shfl_sync(PV_FULL, e.x, 0), o0 = __shfl_sync(PV_FULL, e.y, 0);
+    const int oend = o0 + kk;
+    double g1[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int o = o0 + lane; o < oend; o += 32) gram6(resolve_obs(g, tcam, o, k), g1);
+    warp_reduce_all(g1);
+    double R1[6], v[3];
+    const int fb = resolve_pass1(g1, R1, v);  // identical in every lane
+    bool full = true;
+    if (fb == 1) {
+      const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
+      double s2[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int o = o0 + lane; o < oend; o += 32) gram_pass2(resolve_obs(g, tcam, o, k), R1, id, s2);
+      warp_reduce_all(s2);
+      full = cqr2_solve(R1, s2, v);
+    } else if (fb == 2) {
+      if (lane == 0) {
+        fallback = 1;
+        double Rg[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int o = o0; o < oend; ++o) {
+          const Rows4 rw = resolve_obs(g, tcam, o, k);
+          for (int r = 0; r < 4; ++r) givens_row(Rg, rw.a[r][0], rw.a[r][1], rw.a[r][2], rw.c[r]);
+        }
+        full = lsq_from_r(Rg, 1e-10, v);
+      }
+      full = __shfl_sync(PV_FULL, (int)full, 0);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) v[i] = __shfl_sync(PV_FULL, v[i], 0);
+    }
+    double4 x;
+    if (lane == 0) {
+      resolve_store(l, g1, v, full, tlm, lvr, lbl, x);
+      rankdef = !full;
+    }
+    x.x = __shfl_sync(PV_FULL, x.x, 0);
+    x.y = __shfl_sync(PV_FULL, x.y, 0);
+    x.z = __shfl_sync(PV_FULL, x.z, 0);
+    x.w = __shfl_sync(PV_FULL, x.w, 0);
+    for (int o = o0 + lane; o < oend; o += 32) cost += rows_cost(resolve_obs(g, tcam, o, k), x);
+  } else if (e.x >= 0) {
+    const int l = e.x, o0 = e.y, oend = e.y + kk;
+    double g1[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int o = o0; o < oend; ++o) gram6(resolve_obs(g, tcam, o, k), g1);
+    double R1[6], v[3];
+    const int fb = resolve_pass1(g1, R1, v);
+    bool full = true;
+    if (fb == 1) {
+      const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
+      double s2[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int o = o0; o < oend; ++o) gram_pass2(resolve_obs(g, tcam, o, k), R1, id, s2);
+      full = cqr2_solve(R1, s2, v);
+    } else if (fb == 2) {
+      fallback = 1;
+      double Rg[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int o = o0; o < oend; ++o) {
+        const Rows4 rw = resolve_obs(g, tcam, o, k);
+        for (int r = 0; r < 4; ++r) givens_row(Rg, rw.a[r][0], rw.a[r][1], rw.a[r][2], rw.c[r]);
+      }
+      full = lsq_from_r(Rg, 1e-10, v);
+    }
+    double4 x;
+    resolve_store(l, g1, v, full, tlm, lvr, lbl, x);
+    rankdef = !full;
+    for (int o = o0; o < oend; ++o) cost += rows_cost(resolve_obs(g, tcam, o, k), x);
+  }
+  const unsigned bal = __ballot_sync(PV_FULL, rankdef);
+  const unsigned bfb = __ballot_sync(PV_FULL, fallback);
+  if (lane == 0) {
+    if (bal) atomicAdd(flags + F_N_RANKDEF, __popc(bal));
+    if (bfb) atomicAdd(flags + F_N_FALLBACK, __popc(bfb));
+  }
+  cost = warp_sum(cost);
+  if (lane == 0) part[w] = cost;
 }
 
 // fixed-order two-level sum of warp partials: k_sum2<<<nb, 1024>>> writes one value
