@@ -73,7 +73,8 @@ struct pv_ctx {
   // host copies kept for re-blocking (pv_set_option PV_OPT_BLOCK_BYTES)
   std::vector<int> h_ls_cam, h_ls_lid, h_task_desc;
   std::vector<int> blk_task;  // [n_blk+1] task boundaries of the landmark blocks
-  std::vector<int> blk_obs;   // [n_blk+1] landmark-sorted observation boundaries of the blocks
+  std::vector<int> blk_s;     // [n_blk+1] boundaries of the blocks' partials s (s positions)
+  size_t sbuf_doubles = 0;
   std::vector<int> h_lm_off;  // [n_ls+1]
   // landmark-reduce work (k_lm_reduce): per block, landmarks bucketed by track length
   std::vector<int> blk_ktask;  // [n_blk+1] warp slots
@@ -95,7 +96,7 @@ struct pv_ctx {
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
-  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam, *tarr, *cs_x, *sbuf;
+  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam, *tarr, *cs_x, *sbuf = nullptr;
   double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
   int* flags;
   unsigned* ticket;
@@ -361,26 +362,27 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
   c->sync();
 }
 
-// Work of the landmark reduce (k_lm_reduce, pv_kernels.cuh): per landmark block, the
-// landmarks bucketed by track length k, laid out as 32-entry warp slots of
-// {landmark, first observation, k} (one dependent load per lane).  A short slot holds up
-// to 32 landmarks of equal k <= 32 (one lane each, a k-step serial sum; unused lanes
-// have landmark -1); a long landmark (k > 32) fills a slot alone (one warp).  Longest
-// first, so the grid's tail is made of short slots.
-static void build_ktasks(pv_ctx* c) {
+// Work of the landmark reduce (k_lm_reduce, pv_kernels.cuh) and of the lane-per-landmark
+// re-solve, and the layout of the per-observation partials s.  Per landmark block, the
+// landmarks are bucketed by track length k and laid out as 32-entry warp slots of
+// {landmark, first landmark-sorted observation, k, s position}: a short slot holds up to
+// 32 landmarks of equal k <= 32 (one lane each; unused lanes have landmark -1); a long
+// landmark (k > 32) fills a slot alone.  Longest first, so a grid's tail is made of short
+// slots.  The partials s of a short slot are interleaved -- observation i of lane q at
+// base + 32 i + q -- so the reduce's k-step walk reads 1 KB contiguous per warp load; a
+// long landmark's partials are contiguous.  cs_ls holds the landmark-sorted position of
+// every camera-sorted observation; the camera kernels scatter s to g.cs_pos = its
+// s position.
+static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls) {
   const int B = c->n_blk;
   const std::vector<int>& off = c->h_lm_off;
   std::vector<int4> kl;
   kl.reserve((size_t)c->n_ls + 64 * (size_t)B);
+  std::vector<int> spos((size_t)c->n_os + 1, 0);  // s position of each landmark-sorted obs
+  int64_t sn = 0;                                 // s entries so far
   c->blk_ktask.assign(B + 1, 0);
+  c->blk_s.assign(B + 1, 0);
   std::vector<std::vector<int>> bucket(33);
-  constexpr int SL = 32 / LG;  // landmarks per short slot (each entry repeated LG times)
-  auto slot = [&](const int* ls, int n, int k) {
-    for (int q = 0; q < 32; ++q) {
-      const int i = q / LG;
-      kl.push_back(i < n ? make_int4(ls[i], off[ls[i]], k, 0) : make_int4(-1, 0, k, 0));
-    }
-  };
   for (int b = 0; b < B; ++b) {
     const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
     const int l0 = t0 < c->n_tasks ? c->h_task_desc[4 * t0 + 2] : c->n_ls;
@@ -398,21 +400,49 @@ static void build_ktasks(pv_ctx* c) {
                      [](const std::pair<int, int>& a, const std::pair<int, int>& x) {
                        return a.first > x.first;
                      });
-    for (auto& kvl : longs) {  // a long landmark fills a slot alone: entry 0, rest empty
-      kl.push_back(make_int4(kvl.second, off[kvl.second], kvl.first, 0));
-      for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, kvl.first, 0));
+    for (auto& kvl : longs) {  // entry 0, rest empty; contiguous partials
+      const int k = kvl.first, l = kvl.second;
+      kl.push_back(make_int4(l, off[l], k, (int)sn));
+      for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, k, 0));
+      for (int i = 0; i < k; ++i) spos[off[l] + i] = (int)(sn + i);
+      sn += k;
     }
     for (int k = 32; k >= 0; --k) {
       const std::vector<int>& v = bucket[k];
-      for (size_t i = 0; i < v.size(); i += SL)
-        slot(v.data() + i, (int)std::min<size_t>(SL, v.size() - i), k);
+      for (size_t i = 0; i < v.size(); i += 32) {
+        const int n = (int)std::min<size_t>(32, v.size() - i);
+        for (int q = 0; q < 32; ++q) {
+          if (q < n) {
+            const int l = v[i + q];
+            kl.push_back(make_int4(l, off[l], k, (int)(sn + q)));
+            for (int j = 0; j < k; ++j) spos[off[l] + j] = (int)(sn + q + 32 * j);
+          } else {
+            kl.push_back(make_int4(-1, 0, k, 0));
+          }
+        }
+        sn += 32 * (int64_t)k;
+      }
     }
+    if (sn >= (int64_t)INT32_MAX) throw PvError(PV_EINVAL, "too many partial slots for int32");
     c->blk_ktask[b + 1] = (int)(kl.size() / 32);
+    c->blk_s[b + 1] = (int)sn;
   }
   free_tracked(c, c->d_klist, c->klist_bytes);
   c->d_klist = c->alloc<int4>(kl.size());
   c->klist_bytes = std::max<size_t>(kl.size(), 1) * sizeof(int4);
   CK(cudaMemcpyAsync(c->d_klist, kl.data(), kl.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                     c->stream));
+  // the partials buffer holds every slot's entries (padding lanes included)
+  const size_t need = std::max<size_t>((size_t)sn, 1) * 4;
+  if (need > c->sbuf_doubles) {
+    free_tracked(c, c->sbuf, c->sbuf_doubles * sizeof(double));
+    c->sbuf = c->alloc<double>(need);
+    c->sbuf_doubles = need;
+  }
+  // s position of every camera-sorted observation (the scatter target of W^T v)
+  std::vector<int> cs_s(cs_ls.size(), 0);
+  for (int p = 0; p < c->n_os; ++p) cs_s[p] = spos[cs_ls[p]];
+  CK(cudaMemcpyAsync(c->d_cs_pos, cs_s.data(), cs_s.size() * sizeof(int), cudaMemcpyHostToDevice,
                      c->stream));
   c->sync();
 }
@@ -483,10 +513,8 @@ static void build_blocks(pv_ctx* c) {
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
-  c->blk_obs.assign(B + 1, 0);
-  for (int b = 0; b < B; ++b) c->blk_obs[b + 1] = obs_blk_end[b];
   build_pipe_items(c, seg);
-  build_ktasks(c);
+  build_ktasks(c, cs_pos);  // replaces d_cs_pos (landmark-sorted positions) by s positions
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -497,7 +525,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->lvr = c->alloc<double>(nl * 8);
   c->tarr = c->alloc<double>(nl * 4);  // t per landmark
   c->cs_x = c->alloc<double>(((size_t)c->n_os + 128) * 4);
-  c->sbuf = c->alloc<double>((size_t)c->n_os * 4);
+  // c->sbuf: sized by build_ktasks (slot layout, padding lanes included)
   c->lbl = c->alloc<double>(nl * 4);
   c->ldl = c->alloc<double>(nl * 4);
   c->tlm = c->alloc<double>(nl * 4);
@@ -644,8 +672,8 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca0) {
   // never drop lines this kernel itself writes (its W^T v pass scatters into blocks [a_lo, a_hi))
   const bool writes_db = HA && db >= ca.a_lo && db < ca.a_hi;
   if (db >= 0 && db < c->n_blk && c->tune.discard_s && !writes_db) {
-    ca.disc_lo = c->blk_obs[db];
-    ca.disc_hi = c->blk_obs[db + 1];
+    ca.disc_lo = c->blk_s[db];
+    ca.disc_hi = c->blk_s[db + 1];
   }
   // the persistent kernel runs one warp per camera: with wpc == 1 it reproduces k_cam's
   // summation order bit for bit, so every path (fused, sharded, blocked) stays consistent

@@ -50,7 +50,8 @@ struct Graph {
   const int* lm_off;     // [n_l+1]
   const int4* task;      // [n_tasks] {o0, n, l0, segment-head mask}
   const int* cs_lm;      // [n_o] local landmark of each camera-sorted observation
-  const int* cs_pos;     // [n_o] landmark-sorted position of each camera-sorted observation
+  const int* cs_pos;     // [n_o] s position (partials layout, build_ktasks) of each
+                         // camera-sorted observation
   int n_blk;             // landmark blocks of the L2-blocked term
   const int* seg;        // [n_blk*n_p+1] start of segment (block b, camera c) at b*n_p+c in the
                          // block-major camera-sorted order (block, camera, landmark)
@@ -715,10 +716,7 @@ __device__ __forceinline__ void lr_long(const Task& t, int lane, const double* _
   if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
-#ifndef PV_LR_G
-#define PV_LR_G 1
-#endif
-constexpr int LG = PV_LR_G;  // lanes per landmark in a short warp slot (1, 2, 4, 8)
+constexpr int LG = 1;  // lanes per landmark in a short warp slot (the s layout assumes 1)
 
 template <int STAGE, int MODE>
 __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klist,
@@ -742,7 +740,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
   if (k > 32) {
     Task t;
     t.l0 = __shfl_sync(PV_FULL, e.x, 0);
-    t.o0 = __shfl_sync(PV_FULL, e.y, 0);
+    t.o0 = __shfl_sync(PV_FULL, e.w, 0);  // contiguous partials
     t.n = k;
     t.long_task = true;
     t.heads = 1u;
@@ -758,10 +756,10 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
   if (j == 0) pre = lm_prefetch<STAGE, MODE>(e.x, lrec, lsys, lbl);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (MODE != LR_RHS) {
-    const double* sp = sbuf + 4 * (size_t)e.y;
+    const double* sp = sbuf + 4 * (size_t)e.w;  // interleaved: observation i at + 32 i
 #pragma unroll 4
     for (int i = j; i < k; i += LG) {
-      const double4 v = ldg4p(sp + 4 * i, pf);
+      const double4 v = ldg4p(sp + 128 * (size_t)i, pf);
       acc[0] += v.x;
       acc[1] += v.y;
       acc[2] += v.z;
