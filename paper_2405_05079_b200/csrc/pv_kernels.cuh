@@ -380,11 +380,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       }
       cp_wait<0>();
     }
-    warp_reduce_all(acc);
-    double mine = 0.0;
-#pragma unroll
-    for (int i = 0; i < 12; ++i)
-      if (lane == i) mine = acc[i];
+    double mine = warp_reduce12_lane(acc, lane);
     if (wpc > 1) {  // fixed-order combination over the camera's warps
       if (lane < 12) gred[warp][lane] = mine;
       __syncthreads();

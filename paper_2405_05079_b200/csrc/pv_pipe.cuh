@@ -260,11 +260,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
           }
         }
         if (fl & PF_LAST) {  // camera done: fixed-order warp reduction, write y
-          warp_reduce_all(acc);
-          double mine = 0.0;
-#pragma unroll
-          for (int i = 0; i < 12; ++i)
-            if (lane == i) mine = acc[i];
+          const double mine = warp_reduce12_lane(acc, lane);
           if (lane < 12) {
             double* yp = cy + (size_t)cam * 12 + lane;
             *yp = first_c ? mine : *yp + mine;
