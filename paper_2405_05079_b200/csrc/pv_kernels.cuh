@@ -1769,12 +1769,19 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
     x.z = __shfl_sync(PV_FULL, x.z, 0);
     x.w = __shfl_sync(PV_FULL, x.w, 0);
     for (int o = o0 + lane; o < oend; o += 32) cost += rows_cost(resolve_obs(g, tcam, o, k), x);
-  } else if (e.x >= 0) {
-    const int l = e.x, o0 = e.y, oend = e.y + kk;
+  } else {
+    const bool act = e.x >= 0;
+    const int l = e.x, o0 = e.y, oend = act ? e.y + kk : e.y;
     double g1[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int o = o0; o < oend; ++o) gram6(resolve_obs(g, tcam, o, k), g1);
-    double R1[6], v[3];
-    const int fb = resolve_pass1(g1, R1, v);
+    double cc = 0.0;  // c^T c, for the cost at the solution from the Gram (below)
+    for (int o = o0; o < oend; ++o) {
+      const Rows4 rw = resolve_obs(g, tcam, o, k);
+      gram6(rw, g1);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cc = fma(rw.c[r], rw.c[r], cc);
+    }
+    double R1[6], v[3] = {0.0, 0.0, 0.0};
+    const int fb = act ? resolve_pass1(g1, R1, v) : 0;
     bool full = true;
     if (fb == 1) {
       const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
@@ -1790,10 +1797,38 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
       }
       full = lsq_from_r(Rg, 1e-10, v);
     }
-    double4 x;
-    resolve_store(l, g1, v, full, tlm, lvr, lbl, x);
-    rankdef = !full;
-    for (int o = o0; o < oend; ++o) cost += rows_cost(resolve_obs(g, tcam, o, k), x);
+    double4 x = make_double4(0.0, 0.0, 0.0, 0.0);
+    bool safe = true;
+    if (act) {
+      resolve_store(l, g1, v, full, tlm, lvr, lbl, x);
+      rankdef = !full;
+      // cost at x from the Gram: ||A x + c w||^2 = x^T G x + 2 w x^T (A^T c) + w^2 c^T c.
+      // Used when it does not cancel (cost >= 1e-3 of the terms' magnitude: relative error
+      // <~ 1e-12); otherwise the observations are walked again, by the whole warp.
+      const double gx0 = fma(g1[0], x.x, fma(g1[1], x.y, g1[2] * x.z));
+      const double gx1 = fma(g1[1], x.x, fma(g1[3], x.y, g1[4] * x.z));
+      const double gx2 = fma(g1[2], x.x, fma(g1[4], x.y, g1[5] * x.z));
+      const double t1 = fma(x.x, gx0, fma(x.y, gx1, x.z * gx2));
+      const double t2 = 2.0 * x.w * fma(x.x, g1[6], fma(x.y, g1[7], x.z * g1[8]));
+      const double t3 = x.w * x.w * cc;
+      const double cg = t1 + t2 + t3;
+      safe = cg >= 1e-3 * (fabs(t1) + fabs(t2) + t3);
+      if (safe) cost = cg;
+    }
+    unsigned walk = __ballot_sync(PV_FULL, !safe);
+    while (walk) {  // warp-cooperative walks, lowest lane first (fixed order)
+      const int u = __ffs(walk) - 1;
+      walk &= walk - 1;
+      const int uo = __shfl_sync(PV_FULL, o0, u);
+      double4 xu;
+      xu.x = __shfl_sync(PV_FULL, x.x, u);
+      xu.y = __shfl_sync(PV_FULL, x.y, u);
+      xu.z = __shfl_sync(PV_FULL, x.z, u);
+      xu.w = __shfl_sync(PV_FULL, x.w, u);
+      const double cu = lane < kk ? rows_cost(resolve_obs(g, tcam, uo + lane, k), xu) : 0.0;
+      const double su = warp_sum(cu);
+      if (lane == u) cost = su;
+    }
   }
   const unsigned bal = __ballot_sync(PV_FULL, rankdef);
   const unsigned bfb = __ballot_sync(PV_FULL, fallback);
