@@ -196,6 +196,41 @@ __device__ __forceinline__ double warp_reduce12_lane(const double (&acc)[12], in
   return __shfl_sync(PV_FULL, g, (2 * lane) & 31);
 }
 
+// Same for 32 values: lane i returns the warp sum of component i (bit-identical to
+// warp_reduce_all, ~100 instead of ~480 instructions).
+__device__ __forceinline__ double warp_reduce32_lane(const double (&acc)[32], int lane) {
+  double b[16];
+  const bool h16 = lane & 16;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const double r = __shfl_xor_sync(PV_FULL, h16 ? acc[j] : acc[j + 16], 16);
+    b[j] = (h16 ? acc[j + 16] : acc[j]) + r;
+  }
+  double c[8];
+  const bool h8 = lane & 8;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double r = __shfl_xor_sync(PV_FULL, h8 ? b[j] : b[j + 8], 8);
+    c[j] = (h8 ? b[j + 8] : b[j]) + r;
+  }
+  double e[4];
+  const bool h4 = lane & 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double r = __shfl_xor_sync(PV_FULL, h4 ? c[j] : c[j + 4], 4);
+    e[j] = (h4 ? c[j + 4] : c[j]) + r;
+  }
+  double f[2];
+  const bool h2 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double r = __shfl_xor_sync(PV_FULL, h2 ? e[j] : e[j + 2], 2);
+    f[j] = (h2 ? e[j + 2] : e[j]) + r;
+  }
+  const bool h1 = lane & 1;
+  return (h1 ? f[1] : f[0]) + __shfl_xor_sync(PV_FULL, h1 ? f[0] : f[1], 1);
+}
+
 // ---------------------------------------------------------------------------
 // observation generators
 

@@ -1037,15 +1037,10 @@ __global__ void __launch_bounds__(FT, 2) k_lin_cam(Graph g, const double* __rest
     n1 = n2;
   }
   cp_wait<0>();
-  // fixed-order block reduction (per group)
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1)
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] += __shfl_xor_sync(PV_FULL, acc[i], d);
+  // fixed-order block reduction (per group): warp sums (lane i holds component i), then
+  // the group's warps in order
   const int lane = tid & 31, wq = tid >> 5;
-  if (lane == 0)
-#pragma unroll
-    for (int i = 0; i < 32; ++i) red[wq * 32 + i] = acc[i];
+  red[wq * 32 + lane] = warp_reduce32_lane(acc, lane);
   __syncthreads();
   if (tid < NA) {
     // tot layout: [0,10) w0, [10,20) w1, [20,30) w2, [30,40) w3, [40,52) b_p
