@@ -76,3 +76,26 @@ def test_pipe_lm_trace_matches_reference(pv):
     np.testing.assert_allclose(c, ref, rtol=1e-6, atol=0)
     assert "".join("a" if y < x else "r" for x, y in zip(c, c[1:])) == \
         "".join("a" if y < x else "r" for x, y in zip(ref, ref[1:]))
+
+
+def test_pipe_long_work_lists_large(pv):
+    """The large config with 8 MB landmark blocks: one warp per camera, ~75 work items per
+    warp (the descriptor window of k_cam_pipe shifts several times); the pipelined camera
+    pass must reproduce k_cam bit for bit through a power solve and back-substitution."""
+    from paper_2405_05079_b200 import _lib, synth
+    problem, _ = synth.make_problem("large", 0)
+    dp = pv.DeviceProblem(problem, 0.1)
+    dp.set_option(_lib.PV_OPT_BLOCK_BYTES, 8 << 20)
+    dp.set_state(synth.random_state(problem, 1))
+    dp.linearize(1)
+    dp.damp(1e-4, False)
+    assert dp.info()["warps_per_cam"] == 1 and dp.info()["blocks"] > 10
+    out = []
+    for v in (0, 1):
+        dp.set_option(_lib.PV_OPT_CAM_PIPE, v)
+        order, trunc = dp.power_solve(4, 0.0)
+        dx, dl = dp.step(1)
+        out.append((order, trunc, dx.copy(), dl.copy()))
+    assert out[0][0] == out[1][0] == 4 and out[0][1] == out[1][1]
+    np.testing.assert_array_equal(out[0][2], out[1][2])
+    np.testing.assert_array_equal(out[0][3], out[1][3])
