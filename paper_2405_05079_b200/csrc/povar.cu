@@ -582,8 +582,14 @@ static int op_linearize(pv_ctx* c) {
   CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
   k_build_csx<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x);
   if (!(S == 1 && c->lm_lin_fresh)) {
-    k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr, c->lbl,
-                                                        c->flags, c->coef);
+    if (c->tune.resolve_slots) {  // the lane-per-landmark slot kernels (same knob)
+      const int ns = c->blk_ktask[c->n_blk];
+      k_lin_lm_slots<S><<<blocks_for((long long)ns * 32, 256), 256, 0, c->stream>>>(
+          c->g, c->d_klist, ns, c->crec, c->lrec, c->lvr, c->lbl, c->flags, c->coef);
+    } else {
+      k_lin_lm<S><<<c->nblk_tasks(), 256, 0, c->stream>>>(c->g, c->crec, c->lrec, c->lvr,
+                                                          c->lbl, c->flags, c->coef);
+    }
     c->launched();
   }
   c->lm_lin_fresh = false;

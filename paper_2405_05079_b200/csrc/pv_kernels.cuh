@@ -856,6 +856,55 @@ __device__ __forceinline__ void lin_lm_finish(int l, const double (&acc)[9],
   st4(lbl + (size_t)l * 4, make_double4(acc[6], acc[7], acc[8], 0.0));
 }
 
+// Same, over the k-bucketed warp slots of the landmark reduce (build_ktasks): one lane
+// per landmark walks its k <= 32 observations serially (no shuffle trees; the landmark's
+// Householder basis is built once per lane); a long landmark's slot is reduced by the
+// whole warp.  The per-landmark sums run in a different (fixed) order than k_lin_lm's.
+template <int STAGE>
+__global__ void __launch_bounds__(256) k_lin_lm_slots(Graph g, const int4* __restrict__ klist,
+                                                      int n_slots,
+                                                      const double* __restrict__ crec,
+                                                      const double* __restrict__ lrec,
+                                                      double* __restrict__ lvr,
+                                                      double* __restrict__ lbl, int* flags,
+                                                      Coef k) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_slots) return;
+  const int4 e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k, -}
+  const int kk = e.z;                                     // warp-uniform
+  double acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
+  double h[4] = {0.0, 0.0, 0.0, 0.0};
+  if (kk > 32) {
+    const int l = __shfl_sync(PV_FULL, e.x, 0), o0 = __shfl_sync(PV_FULL, e.y, 0);
+    const double4 x = ldg4(lrec + (size_t)l * LREC);
+    if (STAGE == 2) {
+      const double xv[4] = {x.x, x.y, x.z, x.w};
+      householder_h<4>(xv, h);
+    }
+    for (int o = o0 + lane; o < o0 + kk; o += 32) {
+      const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+      lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, h, k, acc, flags);
+    }
+    warp_reduce_all(acc);
+    if (lane == 0) lin_lm_finish(l, acc, lvr, lbl);
+    return;
+  }
+  if (e.x < 0) return;
+  const double4 x = ldg4(lrec + (size_t)e.x * LREC);
+  if (STAGE == 2) {
+    const double xv[4] = {x.x, x.y, x.z, x.w};
+    householder_h<4>(xv, h);
+  }
+  for (int o = e.y; o < e.y + kk; ++o) {
+    const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
+    lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, h, k, acc, flags);
+  }
+  lin_lm_finish(e.x, acc, lvr, lbl);
+}
+
 template <int STAGE>
 __global__ void __launch_bounds__(256) k_lin_lm(Graph g, const double* __restrict__ crec,
                                                 const double* __restrict__ lrec,
