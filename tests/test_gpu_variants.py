@@ -78,7 +78,8 @@ def test_pipe_lm_trace_matches_reference(pv):
         "".join("a" if y < x else "r" for x, y in zip(ref, ref[1:]))
 
 
-def test_pipe_long_work_lists_large(pv):
+@pytest.mark.parametrize("stage", [1, 2])
+def test_pipe_long_work_lists_large(pv, stage):
     """The large config with 8 MB landmark blocks: one warp per camera, ~75 work items per
     warp (the descriptor window of k_cam_pipe shifts several times); the pipelined camera
     pass must reproduce k_cam bit for bit through a power solve and back-substitution."""
@@ -86,15 +87,19 @@ def test_pipe_long_work_lists_large(pv):
     problem, _ = synth.make_problem("large", 0)
     dp = pv.DeviceProblem(problem, 0.1)
     dp.set_option(_lib.PV_OPT_BLOCK_BYTES, 8 << 20)
-    dp.set_state(synth.random_state(problem, 1))
-    dp.linearize(1)
-    dp.damp(1e-4, False)
+    st = synth.random_state(problem, 1)
+    if stage == 2:  # a stage-1 state first, then the lifted projective state
+        st, _ = pv.lm_minimize(problem, st, 1, pv.SolverConfig(max_outer_iterations=2), dp=dp)
+        st = pv.lift_stage1_to_stage2(st)
+    dp.set_state(st)
+    dp.linearize(stage)
+    dp.damp(1e-4, stage == 2)
     assert dp.info()["warps_per_cam"] == 1 and dp.info()["blocks"] > 10
     out = []
     for v in (0, 1):
         dp.set_option(_lib.PV_OPT_CAM_PIPE, v)
         order, trunc = dp.power_solve(4, 0.0)
-        dx, dl = dp.step(1)
+        dx, dl = dp.step(stage)
         out.append((order, trunc, dx.copy(), dl.copy()))
     assert out[0][0] == out[1][0] == 4 and out[0][1] == out[1][1]
     np.testing.assert_array_equal(out[0][2], out[1][2])
