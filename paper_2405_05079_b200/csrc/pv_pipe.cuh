@@ -35,7 +35,7 @@ namespace pv {
 #define PV_PIPE_W 2
 #endif
 #ifndef PV_PIPE_MINB
-#define PV_PIPE_MINB 1
+#define PV_PIPE_MINB 8  // measured: 1.158 vs 1.176 ms per vlarge term with no bound
 #endif
 // The slot refilled at iteration c was consumed at iteration c-1, whose shared-memory
 // reads all fed instructions that have retired (and a __syncwarp) before the TMA is
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (h.y & 3);
     unsigned char* tb = tbuf + (item & 1) * PT_BYTES;
 #pragma unroll
-    for (int r = 0; r < PCH / 32; ++r) {
+    for (int r = 0; r < (PCH + 31) / 32; ++r) {
       const int q = lane + 32 * r;
       if (q >= h.z) continue;
       const double* src = tarr + 4 * (size_t)si[q];
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
           const double4 P0 = cr[0], P1 = cr[1], P2v = cr[2];
           const double4* tq = reinterpret_cast<const double4*>(tbuf + (c & 1) * PT_BYTES);
 #pragma unroll
-          for (int r = 0; r < PCH / 32; ++r) {
+          for (int r = 0; r < (PCH + 31) / 32; ++r) {
             const int q = lane + 32 * r;
             if (q >= n) continue;
             const double4 X = sx[q];
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
       const double4 v0 = cr[3], v1 = cr[4], v2 = cr[5];
       const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (o0 & 3);
 #pragma unroll
-      for (int r = 0; r < PCH / 32; ++r) {
+      for (int r = 0; r < (PCH + 31) / 32; ++r) {
         const int q = lane + 32 * r;
         if (q >= n) continue;
         const double4 X = sx[q];
