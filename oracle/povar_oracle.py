@@ -574,6 +574,35 @@ def lm_minimize(g: Graph, cams, lms, stage: int, *, max_iterations=50, ftol=1e-6
     return log
 
 
+def spectral_check(s: BlockSystem, max_iterations: int = 50000, tol: float = 1e-14) -> float:
+    """Largest eigenvalue of U^-1 W V+ W^T by power iteration on the symmetrized operator
+    U^-1/2 W V+ W^T U^-1/2, starting from the normalized ones vector; stops when the
+    Rayleigh quotient changes by <= tol * max(1, |mu|) (solvers.py:263-295)."""
+    w, q = np.linalg.eigh(s.U)
+    if (w <= 0).any():
+        raise ValueError("pose blocks must be positive-definite")
+    uih = np.einsum("nij,nj,nkj->nik", q, 1.0 / np.sqrt(w), q)
+    n = s.g.n_cameras
+
+    def half(v):
+        return np.einsum("nij,nj->ni", uih, v.reshape(n, -1)).ravel()
+
+    dim = n * s.d_p
+    v = np.full(dim, 1.0 / math.sqrt(dim))
+    mu = 0.0
+    for _ in range(max_iterations):
+        av = half(coupling(s, half(v)))
+        nrm = np.linalg.norm(av)
+        if nrm == 0:
+            return 0.0
+        mu_new = float(v @ av)
+        v = av / nrm
+        if abs(mu_new - mu) <= tol * max(1.0, abs(mu_new)):
+            return mu_new
+        mu = mu_new
+    return mu
+
+
 def dense_reduced_matrix(s: BlockSystem) -> np.ndarray:
     """Materialized U - W V+ W^T for small problems (normal_eq.py:263-283 analogue)."""
     n, d = s.g.n_cameras, s.d_p

@@ -9,7 +9,7 @@ from .types import (BOTH, JOINT, POSE_ONLY, STAGE1, STAGE2, VARPRO, BaProblem, C
                     SolverConfig, StepReport, TraceRecord, solver_label)
 from .solver import (DeviceProblem, SchurSystem, assemble_system, lm_minimize, pcg_schur_solve,
                      power_schur_solve, random_init, riemannian_step, solve_landmarks,
-                     solve_reduced, total_cost)
+                     solve_reduced, spectral_check, total_cost)
 from .riemann import lift_stage1_to_stage2, retract
 
 __version__ = "0.1.0"

@@ -308,6 +308,43 @@ def pcg_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
     return StepReport(dx, dl, its, 0, rel_res, flag)
 
 
+def spectral_check(system: SchurSystem, max_iterations: int = 50000, tol: float = 1e-14
+                   ) -> float:
+    """Largest eigenvalue of U^-1 W V^+ W^T by power iteration (solvers.py:263-295).
+
+    Same algorithm as the reference: the symmetrized similar operator
+    U^-1/2 W V^+ W^T U^-1/2, started from the normalized ones vector, stopped when
+    the Rayleigh quotient moves by <= tol * max(1, |mu|).  Each application runs the
+    coupling round trip W V^+ W^T on the device (the power-series term kernels,
+    ``pv_schur_apply``); the per-camera U^-1/2 blocks (eigh of the damped U blocks,
+    12x12 or 11x11) are applied on the host.  A property check for small systems.
+    """
+    dp, d, n = system.dp, system.pose_width, system.n_cameras
+    U = dp.debug(_lib.PV_DBG_U).reshape(n, 12, 12)[:, :d, :d]
+    w, q = np.linalg.eigh(U)
+    if (w <= 0).any():
+        raise ValueError("pose blocks must be positive-definite")
+    uih = np.einsum("nij,nj,nkj->nik", q, 1.0 / np.sqrt(w), q)
+
+    def half(v):
+        return np.einsum("nij,nj->ni", uih, v.reshape(n, d)).ravel()
+
+    dim = system.pose_dim
+    v = np.full(dim, 1.0 / math.sqrt(dim))
+    mu = 0.0
+    for _ in range(max_iterations):
+        av = half(dp.schur_apply(system.stage, half(v)))
+        nrm = np.linalg.norm(av)
+        if nrm == 0:
+            return 0.0
+        mu_new = float(v @ av)
+        v = av / nrm
+        if abs(mu_new - mu) <= tol * max(1.0, abs(mu_new)):
+            return mu_new
+        mu = mu_new
+    return mu
+
+
 _INNER_SOLVERS = {"power": power_schur_solve, "pcg": pcg_schur_solve}
 
 

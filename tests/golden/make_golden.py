@@ -29,7 +29,10 @@ tiny.bal.gz  -- the tiny config written by the reference's write_bal (parser and
 pipeline_*   -- run_problem summaries / trace CSVs on tiny.bal.gz
     (povar + ripoba full, iterative stage 1).
 
-``python tests/golden/make_golden.py pcg|bal`` regenerates one group only.
+spectral.npz -- spectral_check (solvers.py:263-295) on the mini systems, with the dense top
+    eigenvalue of U^-1 W V^+ W^T beside it.
+
+``python tests/golden/make_golden.py pcg|bal|spectral`` regenerates one group only.
 """
 
 from __future__ import annotations
@@ -231,6 +234,41 @@ def pcg_arrays(prefix, system):
     return out
 
 
+def make_spectral():
+    """spectral.npz: the reference's spectral_check (solvers.py:263-295) and the dense top
+    eigenvalue of U^-1 W V^+ W^T on the mini systems (stage-1 varpro / joint, stage 2)."""
+    pose = objective.PoseConfig(0.1)
+    out = {}
+    for seed in range(3):
+        d = np.load(OUT / f"mini_{seed}.npz")
+        problem = stratba.BaProblem(int(d["n_cameras"]), int(d["n_landmarks"]),
+                                    len(d["cam_idx"]), d["cam_idx"].astype(np.int64),
+                                    d["lm_idx"].astype(np.int64), d["meas"])
+        st1 = stratba.ProjectiveState(d["cams"], d["lms"])
+        blocks = normal_eq.build_stage1_blocks(problem, st1, pose)
+        systems = [(tag, normal_eq.assemble(blocks, lam, mode))
+                   for lam, mode, tag in ((1e-4, normal_eq.POSE_ONLY, "s1v_"),
+                                          (0.3, normal_eq.BOTH, "s1j_"))]
+        st2 = riemannian.retract(st1)
+        bases = riemannian.state_tangent_bases(st2)
+        raw = normal_eq.build_stage2_blocks(problem, st2)
+        systems.append(("s2_", normal_eq.assemble(riemannian.project_blocks(raw, bases), 1e-3,
+                                                  normal_eq.BOTH)))
+        for tag, system in systems:
+            out[f"m{seed}_{tag}mu"] = solvers.spectral_check(system)
+            out[f"m{seed}_{tag}mu3000"] = solvers.spectral_check(system, max_iterations=3000)
+            u = np.zeros((system.pose_dim, system.pose_dim))
+            d_ = system.u_blocks.shape[1]
+            for i in range(system.n_cameras):
+                u[i * d_:(i + 1) * d_, i * d_:(i + 1) * d_] = system.u_blocks[i]
+            cols = np.stack([solvers._coupling_round_trip(system, e)
+                             for e in np.eye(system.pose_dim)], axis=1)
+            m = np.linalg.solve(u, cols)
+            out[f"m{seed}_{tag}dense"] = float(np.max(np.real(np.linalg.eigvals(m))))
+    np.savez_compressed(OUT / "spectral.npz", **out)
+    print("spectral", {k: v for k, v in out.items() if k.endswith("mu")})
+
+
 def make_pcg():
     pose = objective.PoseConfig(0.1)
     out = {}
@@ -376,6 +414,8 @@ if __name__ == "__main__":
     print("numpy", np.__version__)
     if sys.argv[1:] == ["pcg"]:
         make_pcg()
+    elif sys.argv[1:] == ["spectral"]:
+        make_spectral()
     elif sys.argv[1:] == ["bal"]:
         make_bal()
     else:
