@@ -83,9 +83,11 @@ enum {
                                   one chunk ahead of the compute (0: register gathers)     */
   PV_OPT_CAM_PIPE = 8,         /* 1: single-block camera passes run the persistent kernel
                                   with a TMA-fed shared-memory ring (pv_pipe.cuh)          */
-  PV_OPT_RESOLVE_SLOTS = 9     /* 1: landmark re-solve and landmark-side linearization with
+  PV_OPT_RESOLVE_SLOTS = 9,    /* 1: landmark re-solve and landmark-side linearization with
                                   one lane per landmark (k-bucketed warp slots); 0: warp per
                                   landmark task                                            */
+  PV_OPT_SPLIT_LAST = 10       /* 1: a term's last block runs its W t pass on the pipelined
+                                  kernel and the epilogue + next W^T v pass separately     */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

@@ -108,7 +108,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -729,7 +729,12 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
 template <int S, int EP>
 static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term, double thr,
                             int check_stop) {
-  if (!c->collective()) {
+  if (!c->collective() && c->tune.split_last && c->wpc == 1 && c_hi == c_lo + 1) {
+    // the last block's W t on the pipelined kernel, then the epilogue + next W^T v
+    launch_cam<S, true, EP_NONE, false>(c,
+                                        cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
+    launch_cam<S, false, EP, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, check_stop));
+  } else if (!c->collective()) {
     launch_cam<S, true, EP, true>(c, cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop));
   } else {
     launch_cam<S, true, EP_NONE, false>(c,
@@ -1106,6 +1111,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_RESOLVE_SLOTS:
       c->tune.resolve_slots = value ? 1 : 0;
+      break;
+    case PV_OPT_SPLIT_LAST:
+      c->tune.split_last = value ? 1 : 0;
       break;
     case PV_OPT_CAM_PIPE:
       c->tune.cam_pipe = value ? 1 : 0;

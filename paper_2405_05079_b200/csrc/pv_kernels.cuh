@@ -37,6 +37,7 @@ struct Tune {
   int gather_async;  // k_cam: gather t into shared memory with cp.async one chunk ahead
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
+  int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
