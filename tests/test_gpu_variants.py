@@ -104,3 +104,23 @@ def test_pipe_long_work_lists_large(pv, stage):
     assert out[0][0] == out[1][0] == 4 and out[0][1] == out[1][1]
     np.testing.assert_array_equal(out[0][2], out[1][2])
     np.testing.assert_array_equal(out[0][3], out[1][3])
+
+
+@pytest.mark.parametrize("slots", [0, 1])
+def test_resolve_and_landmark_linearization_variants(pv, slots):
+    """PV_OPT_RESOLVE_SLOTS: lane-per-landmark slots (1, default) or warp-per-task (0) for the
+    landmark re-solve and the landmark side of the linearization; both reproduce the
+    reference's 20-iteration stage-1 trace and its first stage-2 step (tiny config)."""
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    dp = pv.DeviceProblem(problem_from(z), 0.1)
+    dp.set_option(_lib.PV_OPT_RESOLVE_SLOTS, slots)
+    st = pv.ProjectiveState(z["cams"], z["lms"])
+    _, trace = pv.lm_minimize(dp.problem, st, 1, pv.SolverConfig(max_outer_iterations=20),
+                              dp=dp)
+    c = np.array([r.cost for r in trace.records])
+    np.testing.assert_allclose(c, z["s1_costs"], rtol=1e-6, atol=0)
+    rep = pv.riemannian_step(dp.problem, pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"]),
+                             pv.SolverConfig(), dp=dp)
+    assert rep.power_order_used == int(z["s2_it1_order"])
+    assert rel(rep.pose_update, z["s2_it1_dx"]) <= 1e-8
