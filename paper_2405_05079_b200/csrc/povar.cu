@@ -729,11 +729,19 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
 template <int S, int EP>
 static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term, double thr,
                             int check_stop) {
-  if (!c->collective() && c->tune.split_last && c->wpc == 1 && c_hi == c_lo + 1) {
-    // the last block's W t on the pipelined kernel, then the epilogue + next W^T v
-    launch_cam<S, true, EP_NONE, false>(c,
-                                        cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
-    launch_cam<S, false, EP, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, check_stop));
+  if (!c->collective() && c->tune.split_last && c->wpc == 1) {
+    // one warp per camera: the W t pass on the pipelined kernel (a single block) or on k_cam
+    // together with the epilogue (all blocks, the RHS), the epilogue alone (U^-1, x, v,
+    // norms, stop test), then the next W^T v pass of block 0 on the pipelined kernel
+    if (c_hi == c_lo + 1) {
+      launch_cam<S, true, EP_NONE, false>(
+          c, cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
+      launch_cam<S, false, EP, false>(c, cam_args(0, 0, 0, 0, 0, term, thr, check_stop));
+    } else {
+      launch_cam<S, true, EP, false>(c,
+                                     cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
+    }
+    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, 1));
   } else if (!c->collective()) {
     launch_cam<S, true, EP, true>(c, cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop));
   } else {
