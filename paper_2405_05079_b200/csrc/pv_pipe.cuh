@@ -4,9 +4,9 @@
 //
 // Why: in k_cam every warp owns one (camera, block) segment of ~176 observations,
 // i.e. 2-3 staged chunks per phase, so its cp.async double buffer never reaches a
-// steady state: ncu (profiles/r2_ncu_cam_stalls.md) attributes ~60% of the stall
-// samples to the dependent t gathers, the stream waits at the start of each
-// segment and the segment-offset loads.  Here each warp walks a long work list
+// steady state: ncu (profiles/r1_history.md, "Round 1, second session") attributes
+// ~60% of the stall samples to the dependent t gathers, the stream waits at the start
+// of each segment and the segment-offset loads.  Here each warp walks a long work list
 // (the W t chunks of its cameras in block bc, then the W^T v chunks of its cameras
 // in block ba) through a D-deep ring of shared-memory slots:
 //
