@@ -79,8 +79,7 @@ enum {
   PV_OPT_BLOCK_BYTES = 5, /* L2 budget of one landmark block's partials (re-blocks)        */
   PV_OPT_FORCE_COLLECTIVE = 6, /* world == 1: run the sharded code path (split kernels +
                                   ncclAllReduce) over a 1-rank communicator (testing)       */
-  PV_OPT_GATHER_ASYNC = 7,     /* 1: camera kernels gather t into shared memory with cp.async
-                                  one chunk ahead of the compute (0: register gathers)     */
+  PV_OPT_GATHER_ASYNC = 7,     /* no-op (a removed, slower camera-kernel variant)             */
   PV_OPT_CAM_PIPE = 8,         /* 1: single-block camera passes run the persistent kernel
                                   with a TMA-fed shared-memory ring (pv_pipe.cuh)          */
   PV_OPT_RESOLVE_SLOTS = 9,    /* 1: landmark re-solve and landmark-side linearization with

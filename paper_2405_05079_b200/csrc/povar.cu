@@ -641,19 +641,19 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   if (n_deg) *n_deg = fl[F_N_DEGEN];
 }
 
-template <int S, bool HC, int EP, bool HA, bool GA>
+template <int S, bool HC, int EP, bool HA>
 static void launch_cam_v(pv_ctx* c, const CamArgs& ca) {
-  constexpr int smem = GA ? CAM_SMEM_GA : CAM_SMEM;
+  constexpr int smem = CAM_SMEM;
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA, GA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             smem));
     attr_set = true;
   }
   CamArgs a = ca;
   a.wpc = c->wpc;
   const int cams_per_cta = 8 / c->wpc;
-  k_cam<S, HC, EP, HA, GA><<<blocks_for(c->n_p, cams_per_cta), 256, smem, c->stream>>>(
+  k_cam<S, HC, EP, HA><<<blocks_for(c->n_p, cams_per_cta), 256, smem, c->stream>>>(
       c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->cyr, c->cbp, c->cUi, c->cx, c->crhs,
       c->ch, c->nrm, c->ctl, c->host_ctl_dev, c->ticket, c->coef, c->tune, a);
   c->launched();
@@ -688,10 +688,7 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca0) {
     launch_cam_pipe<S, HC, HA>(c, ca);
     return;
   }
-  if (HC && c->tune.gather_async)
-    launch_cam_v<S, HC, EP, HA, true>(c, ca);
-  else
-    launch_cam_v<S, HC, EP, HA, false>(c, ca);
+  launch_cam_v<S, HC, EP, HA>(c, ca);
 }
 
 // landmark half of a term over the landmark blocks [b_lo, b_hi)
@@ -1126,8 +1123,7 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_CAM_PIPE:
       c->tune.cam_pipe = value ? 1 : 0;
       break;
-    case PV_OPT_GATHER_ASYNC:
-      c->tune.gather_async = value ? 1 : 0;
+    case PV_OPT_GATHER_ASYNC:  // removed variant; accepted as a no-op (ABI stability)
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");

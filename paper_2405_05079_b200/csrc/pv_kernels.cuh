@@ -34,7 +34,7 @@ struct Tune {
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
   int discard_s;   // drop consumed s lines from L2 (no write-back)
-  int gather_async;  // k_cam: gather t into shared memory with cp.async one chunk ahead
+  int reserved7;     // (PV_OPT_GATHER_ASYNC: a removed asynchronous-gather k_cam variant)
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
@@ -168,9 +168,6 @@ constexpr int CH = 64;                         // observations per staged chunk
 constexpr int CH_BUF = CH * 32 + CH * 16 + (CH + 8) * 4;  // x, m, ids (one buffer)
 constexpr int CAM_WARP_SMEM = 2 * CH_BUF;      // two buffers per warp
 constexpr int CAM_SMEM = 8 * CAM_WARP_SMEM;    // 8 warps per CTA
-// asynchronous-gather variant: each buffer also holds the gathered t of its chunk
-constexpr int CH_BUF_GA = CH_BUF + CH * 32;
-constexpr int CAM_SMEM_GA = 8 * 2 * CH_BUF_GA;
 
 __device__ __forceinline__ void cp_async16w(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -206,40 +203,6 @@ __device__ __forceinline__ void stage_chunk(unsigned char* buf, int lane, int o,
     cp_async16w(buf + CH * 48 + 16 * lane, ids + a0 + 4 * lane);
 }
 
-// the x / m streams of one chunk (ids staged separately)
-__device__ __forceinline__ void stage_xm(unsigned char* buf, int lane, int o,
-                                         const double* __restrict__ cs_x,
-                                         const double* __restrict__ cs_m) {
-  const char* gx = reinterpret_cast<const char*>(cs_x + 4 * (size_t)o);
-#pragma unroll
-  for (int q = 0; q < (CH * 32) / (16 * 32); ++q)
-    cp_async16w(buf + 16 * (lane + 32 * q), gx + 16 * (lane + 32 * q));
-  const char* gm = reinterpret_cast<const char*>(cs_m + 2 * (size_t)o);
-#pragma unroll
-  for (int q = 0; q < (CH * 16) / (16 * 32); ++q)
-    cp_async16w(buf + CH * 32 + 16 * (lane + 32 * q), gm + 16 * (lane + 32 * q));
-}
-__device__ __forceinline__ void stage_ids(unsigned char* buf, int lane, int o,
-                                          const int* __restrict__ ids) {
-  const int a0 = o & ~3;
-  if (lane < (CH + 8) / 4) cp_async16w(buf + CH * 48 + 16 * lane, ids + a0 + 4 * lane);
-}
-// t_j of every observation of the chunk at o (landmark ids already staged in buf)
-__device__ __forceinline__ void gather_t(unsigned char* buf, int lane, int o, int o_hi,
-                                         const double* __restrict__ tarr, uint64_t pol) {
-  const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o & 3);
-  unsigned char* tb = buf + CH_BUF;
-#pragma unroll
-  for (int r = 0; r < CH / 32; ++r) {
-    const int q = lane + 32 * r;
-    if (o + q < o_hi) {
-      const double* src = tarr + 4 * (size_t)si[q];
-      cp_async16wp(tb + 32 * q, src, pol);
-      cp_async16wp(tb + 32 * q + 16, src + 2, pol);
-    }
-  }
-}
-
 struct CamArgs {
   int c_lo, c_hi;   // landmark-block range of the W t half (HC)
   int first_c;      // 1: overwrite the camera accumulator y, 0: add
@@ -255,7 +218,7 @@ struct CamArgs {
 #ifndef PV_CAM_MINB
 #define PV_CAM_MINB 1
 #endif
-template <int STAGE, bool HC, int EP, bool HA, bool GA>
+template <int STAGE, bool HC, int EP, bool HA>
 __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
     Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
     const double* __restrict__ tarr, double* __restrict__ sbuf, double* __restrict__ cy,
@@ -279,7 +242,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
   const int wpc = ca.wpc;
   const int grp = warp / wpc, gr = warp % wpc;
   const int cam = blockIdx.x * (8 / wpc) + grp;
-  constexpr int SLOT = GA ? CH_BUF_GA : CH_BUF;
+  constexpr int SLOT = CH_BUF;
   unsigned char* wsm = cam_dsm + (size_t)warp * 2 * SLOT;
   const bool valid = cam < g.n_p;
   const bool leader = valid && gr == 0;
@@ -303,59 +266,25 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
       const int nch_all = (o_hi - o_lo + CH - 1) / CH;
       const int nch = nch_all > gr ? (nch_all - gr + wpc - 1) / wpc : 0;  // this warp's chunks
-      if (GA) {
-        // ids run two chunks ahead, x / m / gathered t one chunk ahead (all cp.async):
-        // chunk c computes while the t gathers of chunk c + 1 are in flight
-        if (nch > 0) {
-          stage_ids(wsm, lane, o_lo + gr * CH, g.cs_lm);
-          cp_commit();
-          cp_wait<0>();
-          __syncwarp();
-          stage_xm(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m);
-          gather_t(wsm, lane, o_lo + gr * CH, o_hi, tarr, pt);
-          if (nch > 1) stage_ids(wsm + SLOT, lane, o_lo + (gr + wpc) * CH, g.cs_lm);
-          cp_commit();
-        }
-      } else {
-        if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
-        cp_commit();
-      }
+      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
+      cp_commit();
       for (int c = 0; c < nch; ++c) {
         unsigned char* buf = wsm + (c & 1) * SLOT;
-        if (GA) {
-          cp_wait<0>();
-          __syncwarp();
-          if (c + 1 < nch) {
-            unsigned char* nb = wsm + ((c + 1) & 1) * SLOT;
-            const int on = o_lo + (gr + (c + 1) * wpc) * CH;
-            stage_xm(nb, lane, on, cs_x, g.cs_m);
-            gather_t(nb, lane, on, o_hi, tarr, pt);
-            if (c + 2 < nch) stage_ids(buf, lane, o_lo + (gr + (c + 2) * wpc) * CH, g.cs_lm);
-          }
-          cp_commit();
-        } else {
-          if (c + 1 < nch)
-            stage_chunk(wsm + ((c + 1) & 1) * SLOT, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
-                        g.cs_m, g.cs_lm);
-          cp_commit();
-          cp_wait<1>();
-          __syncwarp();
-        }
+        if (c + 1 < nch)
+          stage_chunk(wsm + ((c + 1) & 1) * SLOT, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
+                      g.cs_m, g.cs_lm);
+        cp_commit();
+        cp_wait<1>();
+        __syncwarp();
         const int o0 = o_lo + (gr + c * wpc) * CH;
         const double4* sx = reinterpret_cast<const double4*>(buf);
         const double2* sm = reinterpret_cast<const double2*>(buf + CH * 32);
         const int* si = reinterpret_cast<const int*>(buf + CH * 48) + (o0 & 3);
         double4 T[CH / 32];
-        if (!GA) {
 #pragma unroll
-          for (int r = 0; r < CH / 32; ++r) {
-            const int q = lane + 32 * r;
-#ifdef PV_EXP_SEQ_GATHER  // timing experiment only: wrong results
-            if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)((o0 + q) % g.n_l), pt);
-#else
-            if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
-#endif
-          }
+        for (int r = 0; r < CH / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
         }
 #pragma unroll
         for (int r = 0; r < CH / 32; ++r) {
@@ -363,7 +292,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
           if (o0 + q < o_hi) {
             const double4 X = sx[q];
             const double2 m = sm[q];
-            const double4 Tq = GA ? reinterpret_cast<const double4*>(buf + CH_BUF)[q] : T[r];
+            const double4 Tq = T[r];
             const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
             double sg[3];
             proj_map<STAGE>(pj, dot4(P0, Tq), dot4(P1, Tq), dot4(P2v, Tq), sg[0], sg[1],
@@ -505,11 +434,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
             sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
             sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
             sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
-#ifdef PV_EXP_SEQ_SCATTER  // timing experiment only: wrong results
-            st4p(sbuf + 4 * (size_t)(o0 + q) + 0 * pos, sv, ps);
-#else
             st4p(sbuf + 4 * (size_t)pos, sv, ps);
-#endif
           }
         }
         __syncwarp();
