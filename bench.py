@@ -245,9 +245,15 @@ def main():
     lam = scfg.initial_lambda
     orders = []
 
+    linearized = [False]
+
     def lm_iteration():
+        # solver.lm_minimize's iteration: a rejected step leaves the state unchanged, so its
+        # linearization (and, POSE_ONLY, the reduced RHS) is reused
         nonlocal f, lam
-        dp.linearize(1)
+        if not linearized[0]:
+            dp.linearize(1)
+            linearized[0] = True
         dp.damp(lam, False)
         order, _ = dp.power_solve(scfg.max_power_order, scfg.power_threshold)
         orders.append(order)
@@ -255,6 +261,7 @@ def main():
         ft = dp.cost(1, trial=True) if ok else math.inf
         if ft < f:
             f, _ = dp.accept(1, resolve=True)
+            linearized[0] = False
             lam = max(scfg.lambda_min, lam * scfg.lambda_decrease)
         else:
             lam = min(scfg.lambda_max, lam * scfg.lambda_increase)

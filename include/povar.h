@@ -85,8 +85,10 @@ enum {
   PV_OPT_RESOLVE_SLOTS = 9,    /* 1: landmark re-solve and landmark-side linearization with
                                   one lane per landmark (k-bucketed warp slots); 0: warp per
                                   landmark task                                            */
-  PV_OPT_SPLIT_LAST = 10       /* 1: a term's last block runs its W t pass on the pipelined
+  PV_OPT_SPLIT_LAST = 10,      /* 1: a term's last block runs its W t pass on the pipelined
                                   kernel and the epilogue + next W^T v pass separately     */
+  PV_OPT_RHS_REUSE = 11        /* 1: a solve after a rejected stage-1 step (same linearization,
+                                  POSE_ONLY) reuses the reduced RHS -(b_p - W V+ b_l)      */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

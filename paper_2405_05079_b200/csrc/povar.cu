@@ -108,10 +108,14 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
+  // reduced RHS reuse: -(b_p - W V+ b_l) depends on the linearization only when V+ is
+  // undamped (POSE_ONLY), so a rejected step's next solve skips its camera pass
+  int64_t lin_id = 0, rhs_lin_id = -1;
+  bool last_damp_both = true;
   int step_stage = 0;
 
   template <class T>
@@ -579,6 +583,7 @@ static void op_cost(pv_ctx* c, int which, double* f) {
 
 template <int S>
 static int op_linearize(pv_ctx* c) {
+  ++c->lin_id;
   CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
   k_build_csx<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x);
   if (!(S == 1 && c->lm_lin_fresh)) {
@@ -623,6 +628,7 @@ static int op_linearize(pv_ctx* c) {
 template <int S>
 static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   const int D = S == 1 ? 12 : 11;
+  c->last_damp_both = both != 0;
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_U, 0, 2 * sizeof(int), c->stream));
   k_damp_cam<<<blocks_for(c->n_p, 64), 64, 0, c->stream>>>((int)c->n_p, D, c->cU, lam, c->cUd,
                                                            c->cUi, c->flags);
@@ -763,6 +769,15 @@ static void launch_term(pv_ctx* c, int i, double thr) {
 }
 
 template <int S>
+static bool rhs_reusable(const pv_ctx* c) {
+  return S == 1 && !c->last_damp_both && c->rhs_lin_id == c->lin_id && c->tune.rhs_reuse;
+}
+template <int S>
+static void mark_rhs(pv_ctx* c) {
+  c->rhs_lin_id = (S == 1 && !c->last_damp_both) ? c->lin_id : -1;
+}
+
+template <int S>
 static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* trunc) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
   CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
@@ -771,8 +786,18 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   // K4: t = V+ b_l for all landmarks, then y = W t over all blocks, the reduced RHS,
   // t_0 = U^-1 rhs and the gather of block 0 (a single pass; blocking does not pay here)
   const int B = c->n_blk;
-  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
-  launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, thr, 0);
+  if (rhs_reusable<S>(c)) {  // t_0 = U^-1 rhs from the stored RHS, then block 0's gather
+    if (!c->collective() && c->tune.split_last && c->wpc == 1) {
+      launch_cam<S, false, EP_RHS_CACHED, false>(c, cam_args(0, 0, 0, 0, 0, 0, thr, 0));
+      launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, thr, 0));
+    } else {
+      launch_cam<S, false, EP_RHS_CACHED, true>(c, cam_args(0, 0, 0, 0, 1, 0, thr, 0));
+    }
+  } else {
+    launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
+    launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, thr, 0);
+    mark_rhs<S>(c);
+  }
   c->check_launch();
   // K5 + K6 terms with a one-term lookahead on the device stop flag
   for (int i = 1; i <= max_order; ++i) {
@@ -820,8 +845,11 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   const int wg = blocks_for((long long)np * 32, 256);  // one warp per camera
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_M, 0, 2 * sizeof(int), c->stream));
   // K4: the reduced RHS (its U^-1 epilogue output is unused here)
-  launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
-  launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, 0.0, 0);
+  if (!rhs_reusable<S>(c)) {
+    launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
+    launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, 0.0, 0);
+    mark_rhs<S>(c);
+  }
   // preconditioner: exact block diagonal and its inverse (solvers.py:161-166)
   k_schur_diag<S><<<wg, 256, 0, c->stream>>>(c->g, c->crec, c->cs_x, c->lsys, c->cmom, c->coef);
   c->launched();
@@ -1116,6 +1144,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_RESOLVE_SLOTS:
       c->tune.resolve_slots = value ? 1 : 0;
+      break;
+    case PV_OPT_RHS_REUSE:
+      c->tune.rhs_reuse = value ? 1 : 0;
       break;
     case PV_OPT_SPLIT_LAST:
       c->tune.split_last = value ? 1 : 0;

@@ -38,6 +38,7 @@ struct Tune {
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
+  int rhs_reuse;     // reuse the reduced RHS across solves of one POSE_ONLY linearization
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -143,7 +144,9 @@ __device__ __forceinline__ void discard_s_lines(double* sbuf, int o_lo, int o_hi
                  : "memory");
 }
 
-enum { EP_NONE = 0, EP_RHS = 1, EP_TERM = 2 };
+// EP_RHS_CACHED: the reduced RHS is already in crhs (same linearization, POSE_ONLY V+):
+// only t_0 = U^-1 rhs and the series start are recomputed
+enum { EP_NONE = 0, EP_RHS = 1, EP_TERM = 2, EP_RHS_CACHED = 3 };
 
 __device__ __forceinline__ void block_sum12(double (&acc)[12], double* red /*[FT/32*12]*/,
                                             double* out /*[12]*/) {
@@ -229,7 +232,8 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
   // ca.wpc warps per camera (1, 2, 4 or 8; 8 / wpc cameras per CTA).  The chunks of a
   // (camera, block) segment are striped over the camera's warps; per-camera sums are
   // combined in fixed order through shared memory.
-  constexpr bool RHS = EP == EP_RHS;
+  constexpr bool RHS = EP == EP_RHS || EP == EP_RHS_CACHED;
+  constexpr bool CACHED = EP == EP_RHS_CACHED;
   constexpr int D = STAGE == 1 ? 12 : 11;
   __shared__ bool last;
   __shared__ double gred[8][12];
@@ -353,7 +357,9 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
         if (lane >= 11) u = 0.0;
       }
       double vin = u;
-      if (RHS) {
+      if (CACHED) {
+        vin = (lane < D && valid) ? crhs[(size_t)cam * 12 + lane] : 0.0;
+      } else if (RHS) {
         const double b = (lane < D && valid) ? cbp[(size_t)cam * 12 + lane] : 0.0;
         vin = lane < D ? -(b - u) : 0.0;
         if (row && valid) crhs[(size_t)cam * 12 + lane] = vin;

@@ -27,9 +27,15 @@ lam = scfg.initial_lambda
 orders, acc = [], []
 
 
+lin = [False]
+
+
 def it():
+    # as solver.lm_minimize / bench.py: re-linearize only after an accepted step
     global f, lam
-    dp.linearize(1)
+    if not lin[0]:
+        dp.linearize(1)
+        lin[0] = True
     dp.damp(lam, False)
     o, _ = dp.power_solve(scfg.max_power_order, scfg.power_threshold)
     orders.append(o)
@@ -37,6 +43,7 @@ def it():
     ft = dp.cost(1, trial=True) if ok else math.inf
     if ft < f:
         f, _ = dp.accept(1, resolve=True)
+        lin[0] = False
         lam = max(scfg.lambda_min, lam * scfg.lambda_decrease)
         acc.append(1)
     else:
