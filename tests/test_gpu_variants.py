@@ -123,3 +123,29 @@ def test_resolve_and_landmark_linearization_variants(pv, slots):
                              pv.SolverConfig(), dp=dp)
     assert rep.power_order_used == int(z["s2_it1_order"])
     assert rel(rep.pose_update, z["s2_it1_dx"]) <= 1e-8
+
+
+@pytest.mark.parametrize("solver", ["power", "pcg"])
+def test_rhs_reuse_after_rejected_step(pv, solver):
+    """PV_OPT_RHS_REUSE: a second solve on the same POSE_ONLY linearization (a rejected step
+    retried with larger damping) reuses the reduced RHS; the steps are bit-identical to
+    recomputing it, and a BOTH-damped solve in between invalidates the reuse."""
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    out = []
+    for reuse in (0, 1):
+        dp = pv.DeviceProblem(problem_from(z), 0.1)
+        dp.set_option(_lib.PV_OPT_RHS_REUSE, reuse)
+        dp.set_state(pv.ProjectiveState(z["cams"], z["lms"]))
+        dp.linearize(1)
+        steps = []
+        for lam, both in ((1e-4, False), (4e-4, False), (1.6e-3, True), (6.4e-3, False)):
+            dp.damp(lam, both)
+            if solver == "power":
+                dp.power_solve(20, 0.01)
+            else:
+                dp.pcg_solve(50, 1e-8)
+            steps.append(np.concatenate(dp.step(1)))
+        out.append(steps)
+    for a, b in zip(*out):
+        np.testing.assert_array_equal(a, b)
