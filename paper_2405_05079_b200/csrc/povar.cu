@@ -80,6 +80,12 @@ struct pv_ctx {
   std::vector<int> blk_ktask;  // [n_blk+1] warp slots
   int4* d_klist = nullptr;
   size_t klist_bytes = 0;
+  // V+ (lsys) and t (tarr) live in warp-slot order: landmark l at slot position h_lpos[l]
+  // (klist entry index), camera-sorted observation o's landmark at d_cs_kpos[o]
+  std::vector<int> h_lpos;
+  int* d_lpos = nullptr;
+  int* d_cs_kpos = nullptr;
+  size_t n_kent = 0;  // klist entries = slot positions (padding lanes included)
   int n_blk = 1;
   int64_t block_bytes = 80ll << 20;
   size_t seg_bytes = 0;
@@ -96,7 +102,8 @@ struct pv_ctx {
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
-  double *crec, *lrec, *lsys, *lvr, *lbl, *ldl, *tlm, *tcam, *tarr, *cs_x, *sbuf = nullptr;
+  double *crec, *lrec, *lvr, *lbl, *ldl, *tlm, *tcam, *cs_x;
+  double *lsys = nullptr, *tarr = nullptr, *sbuf = nullptr;
   double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
   int* flags;
   unsigned* ticket;
@@ -264,6 +271,8 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   // padded by one staging chunk (k_cam copies whole chunks)
   c->d_cs_lm = c->alloc<int>((size_t)n_os + 128);
   c->d_cs_pos = c->alloc<int>((size_t)n_os + 128);
+  c->d_cs_kpos = c->alloc<int>((size_t)n_os + 128);
+  c->d_lpos = c->alloc<int>((size_t)n_ls + 1);
   c->d_cs_m = c->alloc<double>(2 * ((size_t)n_os + 128));
   c->sync();  // host vectors go out of scope
   c->h_ls_cam = std::move(ls_cam);
@@ -283,6 +292,7 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   g.cs_lm = c->d_cs_lm;
   g.cs_m = c->d_cs_m;
   g.cs_pos = c->d_cs_pos;
+  g.cs_kpos = c->d_cs_kpos;
 }
 
 // Landmark blocks of the L2-blocked term: contiguous task ranges with ~equal
@@ -377,12 +387,13 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
 // long landmark's partials are contiguous.  cs_ls holds the landmark-sorted position of
 // every camera-sorted observation; the camera kernels scatter s to g.cs_pos = its
 // s position.
-static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls) {
+static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::vector<int>& cs_lm) {
   const int B = c->n_blk;
   const std::vector<int>& off = c->h_lm_off;
   std::vector<int4> kl;
   kl.reserve((size_t)c->n_ls + 64 * (size_t)B);
   std::vector<int> spos((size_t)c->n_os + 1, 0);  // s position of each landmark-sorted obs
+  std::vector<int> lpos((size_t)c->n_ls + 1, 0);  // slot position of each landmark
   int64_t sn = 0;                                 // s entries so far
   c->blk_ktask.assign(B + 1, 0);
   c->blk_s.assign(B + 1, 0);
@@ -406,6 +417,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls) {
                      });
     for (auto& kvl : longs) {  // entry 0, rest empty; contiguous partials
       const int k = kvl.first, l = kvl.second;
+      lpos[l] = (int)kl.size();
       kl.push_back(make_int4(l, off[l], k, (int)sn));
       for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, k, 0));
       for (int i = 0; i < k; ++i) spos[off[l] + i] = (int)(sn + i);
@@ -418,6 +430,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls) {
         for (int q = 0; q < 32; ++q) {
           if (q < n) {
             const int l = v[i + q];
+            lpos[l] = (int)kl.size();
             kl.push_back(make_int4(l, off[l], k, (int)(sn + q)));
             for (int j = 0; j < k; ++j) spos[off[l] + j] = (int)(sn + q + 32 * j);
           } else {
@@ -443,12 +456,43 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls) {
     c->sbuf = c->alloc<double>(need);
     c->sbuf_doubles = need;
   }
-  // s position of every camera-sorted observation (the scatter target of W^T v)
-  std::vector<int> cs_s(cs_ls.size(), 0);
-  for (int p = 0; p < c->n_os; ++p) cs_s[p] = spos[cs_ls[p]];
+  // s position of every camera-sorted observation (the scatter target of W^T v) and the
+  // slot position of its landmark (the gather index of t and V+)
+  std::vector<int> cs_s(cs_ls.size(), 0), cs_k(cs_lm.size(), 0);
+  for (int p = 0; p < c->n_os; ++p) {
+    cs_s[p] = spos[cs_ls[p]];
+    cs_k[p] = lpos[cs_lm[p]];
+  }
   CK(cudaMemcpyAsync(c->d_cs_pos, cs_s.data(), cs_s.size() * sizeof(int), cudaMemcpyHostToDevice,
                      c->stream));
+  CK(cudaMemcpyAsync(c->d_cs_kpos, cs_k.data(), cs_k.size() * sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_lpos, lpos.data(), lpos.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->stream));
+  // V+ and t in slot order; a re-blocking moves a damped V+ to the new positions
+  const size_t nk = std::max<size_t>(kl.size(), 1);
+  std::vector<double> vold;
+  if (c->lsys && !c->h_lpos.empty()) {
+    vold.resize(c->n_kent * LSYS);
+    CK(cudaMemcpyAsync(vold.data(), c->lsys, vold.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  free_tracked(c, c->lsys, c->n_kent * LSYS * sizeof(double));
+  free_tracked(c, c->tarr, c->n_kent * 4 * sizeof(double));
+  c->lsys = c->alloc<double>(nk * LSYS);
+  c->tarr = c->alloc<double>(nk * 4);
+  if (!vold.empty()) {
+    std::vector<double> vnew(nk * LSYS, 0.0);
+    for (int l = 0; l < c->n_ls; ++l)
+      for (int q = 0; q < LSYS; ++q)
+        vnew[(size_t)lpos[l] * LSYS + q] = vold[(size_t)c->h_lpos[l] * LSYS + q];
+    CK(cudaMemcpyAsync(c->lsys, vnew.data(), vnew.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, c->stream));
+  }
+  c->n_kent = nk;
   c->sync();
+  c->h_lpos = std::move(lpos);
 }
 
 static void build_blocks(pv_ctx* c) {
@@ -518,16 +562,15 @@ static void build_blocks(pv_ctx* c) {
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
   build_pipe_items(c, seg);
-  build_ktasks(c, cs_pos);  // replaces d_cs_pos (landmark-sorted positions) by s positions
+  build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
 }
 
 static void alloc_buffers(pv_ctx* c) {
   const size_t np = c->n_p, nl = c->n_ls;
   c->crec = c->alloc<double>(np * CREC);
   c->lrec = c->alloc<double>(nl * LREC);
-  c->lsys = c->alloc<double>(nl * LSYS);
   c->lvr = c->alloc<double>(nl * 8);
-  c->tarr = c->alloc<double>(nl * 4);  // t per landmark
+  // c->lsys, c->tarr: allocated by build_ktasks (warp-slot order)
   c->cs_x = c->alloc<double>(((size_t)c->n_os + 128) * 4);
   // c->sbuf: sized by build_ktasks (slot layout, padding lanes included)
   c->lbl = c->alloc<double>(nl * 4);
@@ -635,7 +678,7 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   c->launched();
   if (both || !c->vp_cached) {
     k_damp_lm<S><<<blocks_for(c->n_ls, 256), 256, 0, c->stream>>>(
-        c->n_ls, c->lvr, c->lbl, c->lrec, c->lsys, lam, both, c->flags);
+        c->n_ls, c->lvr, c->d_lpos, c->lsys, lam, both, c->flags);
     c->launched();
     c->vp_cached = !both;
   }
@@ -1477,12 +1520,13 @@ int pv_debug_get(pv_ctx* c, int which, double* out) {
     }
     case PV_DBG_VPINV:
     case PV_DBG_DEGEN: {
-      auto h = down(c->lsys, nl * LSYS);
+      auto h = down(c->lsys, c->n_kent * LSYS);  // warp-slot order
       for (size_t j = 0; j < nl; ++j) {
+        const size_t k = (size_t)c->h_lpos[j] * LSYS;
         if (which == PV_DBG_VPINV)
-          for (int q = 0; q < 6; ++q) out[j * 6 + q] = h[j * LSYS + q];
+          for (int q = 0; q < 6; ++q) out[j * 6 + q] = h[k + q];
         else
-          out[j] = h[j * LSYS + 6];
+          out[j] = h[k + 6];
       }
       break;
     }

@@ -54,6 +54,8 @@ struct Graph {
   const int* cs_lm;      // [n_o] local landmark of each camera-sorted observation
   const int* cs_pos;     // [n_o] s position (partials layout, build_ktasks) of each
                          // camera-sorted observation
+  const int* cs_kpos;    // [n_o] warp-slot position (build_ktasks) of the landmark of each
+                         // camera-sorted observation: the index of its V+ and t
   int n_blk;             // landmark blocks of the L2-blocked term
   const int* seg;        // [n_blk*n_p+1] start of segment (block b, camera c) at b*n_p+c in the
                          // block-major camera-sorted order (block, camera, landmark)
@@ -270,13 +272,13 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       const int o_hi = __ldg(g.seg + (size_t)b * np + cam + 1);
       const int nch_all = (o_hi - o_lo + CH - 1) / CH;
       const int nch = nch_all > gr ? (nch_all - gr + wpc - 1) / wpc : 0;  // this warp's chunks
-      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_lm);
+      if (nch > 0) stage_chunk(wsm, lane, o_lo + gr * CH, cs_x, g.cs_m, g.cs_kpos);
       cp_commit();
       for (int c = 0; c < nch; ++c) {
         unsigned char* buf = wsm + (c & 1) * SLOT;
         if (c + 1 < nch)
           stage_chunk(wsm + ((c + 1) & 1) * SLOT, lane, o_lo + (gr + (c + 1) * wpc) * CH, cs_x,
-                      g.cs_m, g.cs_lm);
+                      g.cs_m, g.cs_kpos);
         cp_commit();
         cp_wait<1>();
         __syncwarp();
@@ -542,12 +544,12 @@ struct LmPre {  // per-landmark inputs of the landmark epilogue, prefetched befo
 };
 
 template <int STAGE, int MODE>
-__device__ __forceinline__ LmPre lm_prefetch(int l, const double* __restrict__ lrec,
+__device__ __forceinline__ LmPre lm_prefetch(int l, int kp, const double* __restrict__ lrec,
                                              const double* __restrict__ lsys,
                                              const double* __restrict__ lbl) {
   LmPre p;
-  p.va = ldg4(lsys + (size_t)l * LSYS);
-  p.vb = ldg4(lsys + (size_t)l * LSYS + 4);
+  p.va = ldg4(lsys + (size_t)kp * LSYS);
+  p.vb = ldg4(lsys + (size_t)kp * LSYS + 4);
   p.x = (STAGE == 2 || MODE == LR_BACKSUB) ? ldg4(lrec + (size_t)l * LREC)
                                            : make_double4(0.0, 0.0, 0.0, 1.0);
   p.bl = MODE != LR_TERM ? ldg4(lbl + (size_t)l * 4) : make_double4(0.0, 0.0, 0.0, 0.0);
@@ -555,7 +557,7 @@ __device__ __forceinline__ LmPre lm_prefetch(int l, const double* __restrict__ l
 }
 
 template <int STAGE, int MODE>
-__device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const LmPre& p,
+__device__ __forceinline__ void lm_finish(int l, int kp, const double (&acc)[4], const LmPre& p,
                                           double* __restrict__ tarr, double* __restrict__ ldl,
                                           double* __restrict__ tlm, int* __restrict__ flags,
                                           uint64_t pt) {
@@ -579,11 +581,11 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
     double t[3];
     sym3_apply(vp, s3, t);
     if (STAGE == 1) {
-      st4p(tarr + (size_t)l * 4, make_double4(t[0], t[1], t[2], 0.0), pt);
+      st4p(tarr + (size_t)kp * 4, make_double4(t[0], t[1], t[2], 0.0), pt);
     } else {
       double t4[4];
       basis_apply<4>(h, t, t4);
-      st4p(tarr + (size_t)l * 4, make_double4(t4[0], t4[1], t4[2], t4[3]), pt);
+      st4p(tarr + (size_t)kp * 4, make_double4(t4[0], t4[1], t4[2], t4[3]), pt);
     }
     return;
   }
@@ -615,7 +617,8 @@ __device__ __forceinline__ void lm_finish(int l, const double (&acc)[4], const L
 // its own, reduced by the whole warp (coalesced, fixed-order tree).  Deterministic.
 
 template <int STAGE, int MODE>
-__device__ __forceinline__ void lr_long(const Task& t, int lane, const double* __restrict__ sbuf,
+__device__ __forceinline__ void lr_long(const Task& t, int kp, int lane,
+                                        const double* __restrict__ sbuf,
                                         const double* __restrict__ lrec,
                                         double* __restrict__ tarr,
                                         const double* __restrict__ lsys,
@@ -624,7 +627,7 @@ __device__ __forceinline__ void lr_long(const Task& t, int lane, const double* _
                                         uint64_t pt) {
   constexpr int NV = STAGE == 1 ? 3 : 4;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const LmPre pre = lane == 0 ? lm_prefetch<STAGE, MODE>(t.l0, lrec, lsys, lbl) : LmPre{};
+  const LmPre pre = lane == 0 ? lm_prefetch<STAGE, MODE>(t.l0, kp, lrec, lsys, lbl) : LmPre{};
   if (MODE != LR_RHS) {
     double a2[NV];
 #pragma unroll
@@ -641,7 +644,7 @@ __device__ __forceinline__ void lr_long(const Task& t, int lane, const double* _
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = a2[i];
   }
-  if (lane == 0) lm_finish<STAGE, MODE>(t.l0, acc, pre, tarr, ldl, tlm, flags, pt);
+  if (lane == 0) lm_finish<STAGE, MODE>(t.l0, kp, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
 constexpr int LG = 1;  // lanes per landmark in a short warp slot (the s layout assumes 1)
@@ -672,7 +675,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
     t.n = k;
     t.long_task = true;
     t.heads = 1u;
-    lr_long<STAGE, MODE>(t, lane, sbuf, lrec, tarr, lsys, lbl, ldl, tlm, flags, pf, pt);
+    lr_long<STAGE, MODE>(t, 32 * w, lane, sbuf, lrec, tarr, lsys, lbl, ldl, tlm, flags, pf, pt);
     return;
   }
   // LG lanes per landmark (the slot entry is repeated LG times): lane j of a group sums
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
   if (e.x < 0) return;  // whole groups are empty together
   const int j = lane & (LG - 1);
   LmPre pre;
-  if (j == 0) pre = lm_prefetch<STAGE, MODE>(e.x, lrec, lsys, lbl);
+  if (j == 0) pre = lm_prefetch<STAGE, MODE>(e.x, 32 * w + lane, lrec, lsys, lbl);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (MODE != LR_RHS) {
     const double* sp = sbuf + 4 * (size_t)e.w;  // interleaved: observation i at + 32 i
@@ -700,7 +703,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
       for (int c = 0; c < (STAGE == 1 ? 3 : 4); ++c) acc[c] += __shfl_xor_sync(gm, acc[c], d);
     }
   }
-  if (j == 0) lm_finish<STAGE, MODE>(e.x, acc, pre, tarr, ldl, tlm, flags, pt);
+  if (j == 0) lm_finish<STAGE, MODE>(e.x, 32 * w + lane, acc, pre, tarr, ldl, tlm, flags, pt);
 }
 
 // block-major camera-sorted copy of the measurements (once per re-blocking)
@@ -1185,11 +1188,10 @@ __global__ void k_damp_cam(int n_p, int D, const double* __restrict__ cU, double
     }
 }
 
-// K2 damping + V+ (per landmark); also the RHS landmark vector t = V+ b_l
+// K2 damping + V+ (per landmark), stored at the landmark's warp-slot position lpos[l]
 template <int STAGE>
-__global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const double* __restrict__ lbl,
-                          double* __restrict__ lrec, double* __restrict__ lsys, double lam,
-                          int both, int* flags) {
+__global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const int* __restrict__ lpos,
+                          double* __restrict__ lsys, double lam, int both, int* flags) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   bool degen = false;
   if (l < n_l) {
@@ -1227,7 +1229,7 @@ __global__ void k_damp_lm(int n_l, const double* __restrict__ lvr, const double*
     } else {
       degen = pinv_sym3(V6, 1e-10, P6);
     }
-    double* o = lsys + (size_t)l * LSYS;
+    double* o = lsys + (size_t)__ldg(lpos + l) * LSYS;  // warp-slot order
     st4(o, make_double4(P6[0], P6[1], P6[2], P6[3]));
     st4(o + 4, make_double4(P6[4], P6[5], degen ? 1.0 : 0.0, 0.0));
   }

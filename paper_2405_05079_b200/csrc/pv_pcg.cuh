@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_schur_diag(Graph g, const double* __res
     for (int o = o_lo + lane; o < o_hi; o += 32) {
       const double4 X = ldg4(cs_x + 4 * (size_t)o);
       const double2 m = ldg2(g.cs_m + 2 * (size_t)o);
-      const int l = __ldg(g.cs_lm + o);
+      const int l = __ldg(g.cs_kpos + o);  // slot position of V+
       const Gen G = STAGE == 1 ? gen_s1(P0, P1, P2, m.x, m.y, k.s) : gen_s2(P0, P1, P2, X);
       const double4 gr[3] = {G.g0, G.g1, G.g2};
       double gt[3][3];

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
 #endif
       *reinterpret_cast<int4*>(slot + PH_OFF) = make_int4(cam, o, n, fl);
       if (n > 0) {
-        const int* ids = (fl & PF_HA) ? g.cs_pos : g.cs_lm;
+        const int* ids = (fl & PF_HA) ? g.cs_pos : g.cs_kpos;
         const int i0 = o & ~3;
         const int i1 = (o + n + 3) & ~3;
         const unsigned bx = (unsigned)n * 32u, bm = (unsigned)n * 16u,

@@ -149,3 +149,32 @@ def test_rhs_reuse_after_rejected_step(pv, solver):
         out.append(steps)
     for a, b in zip(*out):
         np.testing.assert_array_equal(a, b)
+
+
+def test_reblocking_keeps_damped_landmark_inverse(pv):
+    """V+ and t live in warp-slot order (build_ktasks); a re-blocking after pv_damp
+    (PV_OPT_BLOCK_BYTES) moves V+ to the new slot positions: the debug view is unchanged, and
+    after the re-linearization the re-blocking requires, the solve equals the one on a
+    context blocked that way from the start."""
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    st = pv.ProjectiveState(z["cams"], z["lms"])
+    outs = []
+    for late in (False, True):
+        dp = pv.DeviceProblem(problem_from(z), 0.1)
+        if not late:
+            dp.set_option(_lib.PV_OPT_BLOCK_BYTES, 64 << 10)
+        dp.set_state(st)
+        dp.linearize(1)
+        dp.damp(1e-4, True)
+        vp0 = dp.debug(_lib.PV_DBG_VPINV).copy()
+        if late:
+            dp.set_option(_lib.PV_OPT_BLOCK_BYTES, 64 << 10)
+            np.testing.assert_array_equal(dp.debug(_lib.PV_DBG_VPINV), vp0)
+        assert dp.info()["blocks"] > 1
+        dp.linearize(1)  # a re-blocking drops the camera-sorted copies of the state
+        dp.damp(1e-4, True)
+        np.testing.assert_array_equal(dp.debug(_lib.PV_DBG_VPINV), vp0)
+        dp.power_solve(20, 0.01)
+        outs.append(np.concatenate(dp.step(1)))
+    np.testing.assert_array_equal(outs[0], outs[1])
