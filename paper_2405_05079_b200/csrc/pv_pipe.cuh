@@ -31,11 +31,14 @@ namespace pv {
 #ifndef PV_PIPE_D
 #define PV_PIPE_D 3
 #endif
+// Shape (vlarge LM iteration, tools/lm_iter_time.py; profiles/r1_history.md): 3 warps per
+// CTA, 5 CTAs per SM (15 resident warps, 120 registers) 18.24 ms; 2 x 8 (14 warps, the
+// shared-memory limit) 18.29; ring depth 2 19.06; depth 4 (12 warps) 18.57.
 #ifndef PV_PIPE_W
-#define PV_PIPE_W 2
+#define PV_PIPE_W 3
 #endif
 #ifndef PV_PIPE_MINB
-#define PV_PIPE_MINB 8  // measured: 1.158 vs 1.176 ms per vlarge term with no bound
+#define PV_PIPE_MINB 5
 #endif
 // The slot refilled at iteration c was consumed at iteration c-1, whose shared-memory
 // reads all fed instructions that have retired (and a __syncwarp) before the TMA is
