@@ -649,8 +649,17 @@ __device__ __forceinline__ void lr_long(const Task& t, int kp, int lane,
 
 constexpr int LG = 1;  // lanes per landmark in a short warp slot (the s layout assumes 1)
 
+// build-time tuning of the short-slot walk (loads in flight per lane, resident CTAs)
+#ifndef PV_LR_UNROLL
+#define PV_LR_UNROLL 4
+#endif
+#ifndef PV_LR_MINB
+#define PV_LR_MINB 1
+#endif
+constexpr int kLrUnroll = PV_LR_UNROLL;
+
 template <int STAGE, int MODE>
-__global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klist,
+__global__ void __launch_bounds__(256, PV_LR_MINB) k_lm_reduce(const int4* __restrict__ klist,
                                                    const double* __restrict__ sbuf,
                                                    const double* __restrict__ lrec,
                                                    double* __restrict__ tarr,
@@ -688,7 +697,7 @@ __global__ void __launch_bounds__(256) k_lm_reduce(const int4* __restrict__ klis
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (MODE != LR_RHS) {
     const double* sp = sbuf + 4 * (size_t)e.w;  // interleaved: observation i at + 32 i
-#pragma unroll 4
+#pragma unroll kLrUnroll
     for (int i = j; i < k; i += LG) {
       const double4 v = ldg4p(sp + 128 * (size_t)i, pf);
       acc[0] += v.x;
