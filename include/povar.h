@@ -87,8 +87,10 @@ enum {
                                   landmark task                                            */
   PV_OPT_SPLIT_LAST = 10,      /* 1: a term's last block runs its W t pass on the pipelined
                                   kernel and the epilogue + next W^T v pass separately     */
-  PV_OPT_RHS_REUSE = 11        /* 1: a solve after a rejected stage-1 step (same linearization,
+  PV_OPT_RHS_REUSE = 11,       /* 1: a solve after a rejected stage-1 step (same linearization,
                                   POSE_ONLY) reuses the reduced RHS -(b_p - W V+ b_l)      */
+  PV_OPT_COST_CS = 12          /* 1: pv_cost walks the camera-sorted segments (one camera load
+                                  per warp segment); 0: landmark-task order                */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

@@ -115,7 +115,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -609,10 +609,17 @@ static void op_cost(pv_ctx* c, int which, double* f) {
   const double* lms = which == PV_TRIAL ? c->tlm : c->lrec;
   const int ls = which == PV_TRIAL ? 4 : LREC;
   CK(cudaMemsetAsync(c->flags + F_INVALID_Z, 0, sizeof(int), c->stream));
-  k_cost<S><<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
-      c->g, cams, cs, lms, ls, c->cpart, c->flags, c->coef);
+  int nparts = c->n_tasks;
+  if (c->tune.cost_cs) {  // camera-sorted walk, ~256 observations per warp
+    nparts = (int)std::max<long long>(1, std::min<long long>(c->n_tasks, ((long long)c->n_os + 255) / 256));
+    k_cost_cs<S><<<blocks_for((long long)nparts * 32, 256), 256, 0, c->stream>>>(
+        c->g, cams, cs, lms, ls, nparts, c->cpart, c->flags, c->coef);
+  } else {
+    k_cost<S><<<blocks_for((long long)c->n_tasks * 32, 64), 64, 0, c->stream>>>(
+        c->g, cams, cs, lms, ls, c->cpart, c->flags, c->coef);
+  }
   c->launched();
-  c->sum_partials();
+  c->sum_partials(nparts);
   c->check_launch();
   c->allreduce(c->scal, 1);
   c->allreduce_flags();
@@ -1190,6 +1197,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_RHS_REUSE:
       c->tune.rhs_reuse = value ? 1 : 0;
+      break;
+    case PV_OPT_COST_CS:
+      c->tune.cost_cs = value ? 1 : 0;
       break;
     case PV_OPT_SPLIT_LAST:
       c->tune.split_last = value ? 1 : 0;

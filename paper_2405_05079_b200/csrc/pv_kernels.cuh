@@ -39,6 +39,7 @@ struct Tune {
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
   int rhs_reuse;     // reuse the reduced RHS across solves of one POSE_ONLY linearization
+  int cost_cs;       // cost over the camera-sorted segments (k_cost_cs) instead of k_cost
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -1347,6 +1348,46 @@ __global__ void __launch_bounds__(64) k_cost(Graph g, const double* __restrict__
     }
   }
   warp_partial(acc, part);
+}
+
+// Cost over the block-major camera-sorted observations: warp w takes the observation range
+// [w n_o / nw, (w + 1) n_o / nw) and walks the (block, camera) segments it crosses, so the
+// camera record is one warp-uniform (broadcast) load per segment and only the landmark is
+// gathered per observation (k_cost gathers three camera rows per observation and is
+// L1-bound on them).  One partial per warp, summed in fixed order by k_sum.
+template <int STAGE>
+__global__ void __launch_bounds__(256) k_cost_cs(Graph g, const double* __restrict__ cams,
+                                                 int cstride, const double* __restrict__ lms,
+                                                 int lstride, int nw, double* __restrict__ part,
+                                                 int* flags, Coef k) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nw) return;
+  const int o_begin = (int)((long long)w * g.n_o / nw);
+  const int o_end = (int)((long long)(w + 1) * g.n_o / nw);
+  double acc = 0.0;
+  if (o_begin < o_end) {
+    // last segment starting at or before o_begin
+    int lo = 0, hi = g.n_blk * g.n_p;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(g.seg + mid) <= o_begin) lo = mid; else hi = mid;
+    }
+    int sgi = lo, o = o_begin;
+    while (o < o_end) {
+      const int se = min(__ldg(g.seg + sgi + 1), o_end);
+      const int cam = sgi % g.n_p;
+      for (int q = o + lane; q < se; q += 32) {
+        const double2 m = ldg2(g.cs_m + 2 * (size_t)q);
+        const double4 x = ldg4(lms + (size_t)__ldg(g.cs_lm + q) * lstride);
+        acc += obs_cost<STAGE>(cams, cstride, cam, m.x, m.y, x, k, flags);
+      }
+      o = max(o, se);
+      ++sgi;
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) part[w] = acc;
 }
 
 // ---------------------------------------------------------------------------

@@ -178,3 +178,39 @@ def test_reblocking_keeps_damped_landmark_inverse(pv):
         dp.power_solve(20, 0.01)
         outs.append(np.concatenate(dp.step(1)))
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("block_bytes", [64 << 10, 80 << 20])
+def test_cost_camera_sorted_matches_task_order(pv, block_bytes):
+    """pv_cost over the camera-sorted segments (PV_OPT_COST_CS, k_cost_cs) and over the
+    landmark tasks (k_cost) sum the same per-observation terms in different fixed orders:
+    equal to rounding, and both equal the oracle's total_cost (objective.py:194-211) on the
+    golden starts of tests/golden/tiny_lm.npz."""
+    from oracle import povar_oracle as O
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    starts = {1: (z["cams"], z["lms"]), 2: (z["s2_cams0"], z["s2_lms0"])}
+    g = O.graph_of(problem_from(z))
+    for stage, (cams, lms) in starts.items():
+        want = O.total_cost(g, cams, lms, stage)
+        got = []
+        for knob in (0, 1):
+            dp = pv.DeviceProblem(problem_from(z), 0.1)
+            dp.set_option(_lib.PV_OPT_BLOCK_BYTES, block_bytes)
+            dp.set_option(_lib.PV_OPT_COST_CS, knob)
+            dp.set_state(pv.ProjectiveState(cams, lms))
+            got.append(dp.cost(stage))
+        assert got[1] == pytest.approx(got[0], rel=1e-13, abs=0)
+        assert got[1] == pytest.approx(want, rel=1e-12, abs=0)
+
+
+def test_cost_camera_sorted_degenerate_depth(pv):
+    """A stage-2 observation with |z| <= 1e-12 makes the camera-sorted cost +inf, as
+    total_cost does (objective.py:206-210)."""
+    from paper_2405_05079_b200 import _lib
+    import _kat
+    pr, st, _ = _kat.degenerate_depth_case()
+    dp = pv.DeviceProblem(pr, 0.1)
+    dp.set_option(_lib.PV_OPT_COST_CS, 1)
+    dp.set_state(st)
+    assert dp.cost(2) == np.inf
