@@ -602,6 +602,9 @@ static void alloc_buffers(pv_ctx* c) {
 // ---------------------------------------------------------------------------
 // operations
 
+#ifndef PV_COST_OBS
+#define PV_COST_OBS 512
+#endif
 template <int S>
 static void op_cost(pv_ctx* c, int which, double* f) {
   const double* cams = which == PV_TRIAL ? c->tcam : c->crec;
@@ -610,8 +613,9 @@ static void op_cost(pv_ctx* c, int which, double* f) {
   const int ls = which == PV_TRIAL ? 4 : LREC;
   CK(cudaMemsetAsync(c->flags + F_INVALID_Z, 0, sizeof(int), c->stream));
   int nparts = c->n_tasks;
-  if (c->tune.cost_cs) {  // camera-sorted walk, ~256 observations per warp
-    nparts = (int)std::max<long long>(1, std::min<long long>(c->n_tasks, ((long long)c->n_os + 255) / 256));
+  if (c->tune.cost_cs) {  // camera-sorted walk, ~PV_COST_OBS observations per warp
+    nparts = (int)std::max<long long>(
+        1, std::min<long long>(c->n_tasks, ((long long)c->n_os + PV_COST_OBS - 1) / PV_COST_OBS));
     k_cost_cs<S><<<blocks_for((long long)nparts * 32, 256), 256, 0, c->stream>>>(
         c->g, cams, cs, lms, ls, nparts, c->cpart, c->flags, c->coef);
   } else {
