@@ -37,7 +37,9 @@ enum {
   PV_ECUDA = 2,        /* -> RuntimeError                                                   */
   PV_ENCCL = 3,        /* -> RuntimeError                                                   */
   PV_ENONFINITE = 4,   /* -> NumericFailureError   (solvers.py:336-338)                     */
-  PV_EDEGENERATE = 5   /* -> FloatingPointError    (normal_eq.py:86-87)                     */
+  PV_EDEGENERATE = 5,  /* -> FloatingPointError    (normal_eq.py:86-87)                     */
+  PV_ESINGULAR = 6     /* -> numpy.linalg.LinAlgError (np.linalg.inv of a singular pose
+                          block, solvers.py:108-109)                                       */
 };
 
 enum { PV_CURRENT = 0, PV_TRIAL = 1 };
@@ -79,7 +81,7 @@ enum {
   PV_OPT_BLOCK_BYTES = 5, /* L2 budget of one landmark block's partials (re-blocks)        */
   PV_OPT_FORCE_COLLECTIVE = 6, /* world == 1: run the sharded code path (split kernels +
                                   ncclAllReduce) over a 1-rank communicator (testing)       */
-  PV_OPT_GATHER_ASYNC = 7,     /* no-op (a removed, slower camera-kernel variant)             */
+  /* 7: reserved (a removed camera-kernel variant; rejected as an unknown option)          */
   PV_OPT_CAM_PIPE = 8,         /* 1: single-block camera passes run the persistent kernel
                                   with a TMA-fed shared-memory ring (pv_pipe.cuh)          */
   PV_OPT_RESOLVE_SLOTS = 9,    /* 1: landmark re-solve and landmark-side linearization with
@@ -158,6 +160,11 @@ int pv_accept(pv_ctx* ctx, int stage, int resolve, double* f_new, int64_t* n_ran
 /* closed-form landmarks for the CURRENT cameras with current landmarks as the
  * fallback (solve_landmarks on the current state); result kept as current. */
 int pv_resolve_current(pv_ctx* ctx, int64_t* n_rank_deficient);
+
+/* back_substitute (normal_eq.py:239-250) of a given pose update dx (n_p*d, d = 12 stage 1,
+ * 11 stage 2) on the current damped system: dl = -V+ (b_l + W^T dx), zero for degenerate
+ * landmark blocks.  Replaces the device step (pv_get_step, pv_trial use it afterwards). */
+int pv_back_substitute(pv_ctx* ctx, const double* dx);
 
 /* StepReport arrays of the last pv_power_solve / pv_pcg_solve: dx (n_p*d), dl (n_l*dl) for the
  * whole problem (unobserved / foreign-shard landmarks left untouched). */

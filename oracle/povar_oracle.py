@@ -9,7 +9,7 @@ import it.  The product path (``paper_2405_05079_b200``) never imports it.
 
 Parity pin: ``tests/golden/make_golden.py`` runs the real reference package in
 the build container and stores its outputs as fixtures under ``tests/golden``;
-``tests/test_oracle_golden.py`` checks this module against them.  Numerics are
+``tests/test_oracle.py`` checks this module against them.  Numerics are
 NumPy 2.3 / OpenBLAS (eigh, svd, inv), the same libraries the reference
 calls.
 

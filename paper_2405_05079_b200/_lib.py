@@ -16,7 +16,7 @@ from .types import NumericFailureError
 LIB_PATH = os.environ.get("PV_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libpovar.so")
 
-PV_OK, PV_EINVAL, PV_ECUDA, PV_ENCCL, PV_ENONFINITE, PV_EDEGENERATE = range(6)
+PV_OK, PV_EINVAL, PV_ECUDA, PV_ENCCL, PV_ENONFINITE, PV_EDEGENERATE, PV_ESINGULAR = range(7)
 PV_CURRENT, PV_TRIAL = 0, 1
 (PV_DBG_U, PV_DBG_UINV, PV_DBG_BP, PV_DBG_V, PV_DBG_VPINV, PV_DBG_BL, PV_DBG_DEGEN, PV_DBG_W,
  PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN, PV_DBG_SDIAG, PV_DBG_MINV) = range(14)
@@ -25,7 +25,7 @@ INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "
                "warps_per_cam")
 PV_INFO_COUNT = 16
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
- PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, PV_OPT_GATHER_ASYNC, PV_OPT_CAM_PIPE,
+ PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, _PV_OPT_RESERVED7, PV_OPT_CAM_PIPE,
  PV_OPT_RESOLVE_SLOTS, PV_OPT_SPLIT_LAST, PV_OPT_RHS_REUSE, PV_OPT_COST_CS) = range(13)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
@@ -57,6 +57,7 @@ SIGNATURES = [
     ("pv_trial", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("pv_accept", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _D, _I64]),
     ("pv_resolve_current", ctypes.c_int, [_P, _I64]),
+    ("pv_back_substitute", ctypes.c_int, [_P, _D]),
     ("pv_get_step", ctypes.c_int, [_P, _D, _D]),
     ("pv_schur_apply", ctypes.c_int, [_P, ctypes.c_int, _D, _D]),
     ("pv_bench_terms", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int,
@@ -80,10 +81,31 @@ class PovarLibraryError(RuntimeError):
     """libpovar.so is missing or failed to load (no CPU fallback exists)."""
 
 
+def _preload_nccl() -> None:
+    """Make libnccl.so.2 resolve to PyTorch's bundled NCCL (2.28) before libpovar.so loads.
+
+    libpovar.so and libtorch_cuda.so both need ``libnccl.so.2``; the dynamic loader binds
+    that name to whichever copy is loaded first.  PyTorch needs symbols only 2.28 has, so
+    the system 2.27 must not win when libpovar.so happens to load before ``import torch``.
+    The bundled library is an ABI superset of the 2.27 header libpovar.so is built with.
+    """
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        path = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+            return
+
+
 def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    _preload_nccl()
     if not os.path.exists(LIB_PATH):
         raise PovarLibraryError(
             f"{LIB_PATH} not found: build it with `make` (or __graft_entry__.build()); "
@@ -115,6 +137,9 @@ def check(rc: int, ctx=None) -> None:
         raise NumericFailureError(msg)
     if rc == PV_EDEGENERATE:
         raise FloatingPointError(msg)
+    if rc == PV_ESINGULAR:
+        import numpy as np
+        raise np.linalg.LinAlgError(msg)
     kind = "NCCL" if rc == PV_ENCCL else "CUDA"
     raise RuntimeError(f"libpovar {kind} error ({rc}): {msg}")
 

@@ -2,10 +2,13 @@
 
 * ``parse_bal``            -> bal_io.py:155-203 (pv_bal_header / pv_bal_parse,
                               multi-threaded, same grammar and BalParseError messages)
-* ``load_bal``             -> bal_io.py:229-241 (gzip / bzip2 sniffing on the host)
+* ``load_bal``             -> bal_io.py:229-241 (gzip / bzip2 detected from the leading
+                              bytes, decompressed whole, then the native parser)
 * ``prune_underobserved``  -> bal_io.py:244-278 (distinct-camera counts in
                               pv_bal_prune_masks, O(n_obs) without a sort)
-* ``write_bal``            -> bal_io.py:206-226
+
+Writing BAL files (``write_bal``, bal_io.py:206-226) is not part of this path: the
+reference's writer is used where a file is needed (tests, make_golden.py).
 
 The native library is required (there is no Python fallback); the BAL entry
 points are host-only and run without a GPU.
@@ -13,9 +16,7 @@ points are host-only and run without a GPU.
 
 from __future__ import annotations
 
-import bz2
 import ctypes
-import gzip
 import logging
 from pathlib import Path
 from typing import IO
@@ -76,38 +77,21 @@ def parse_bal(stream: IO[str]) -> BaProblem:
     return parse_bytes(data)
 
 
+# leading bytes of the compressed containers load_bal accepts (bal_io.py:229-241); any
+# other file is read as plain text
+_CODECS = ((b"\x1f\x8b", "gzip"), (b"BZh", "bz2"))
+
+
 def load_bal(path: str | Path) -> BaProblem:
-    """Read a BAL file, transparently decompressing gzip or bzip2 input (bal_io.py:229-241)."""
-    path = Path(path)
-    with open(path, "rb") as fh:
-        magic = fh.read(3)
-    if magic[:2] == b"\x1f\x8b":
-        opener = gzip.open
-    elif magic == b"BZh":
-        opener = bz2.open
-    else:
-        opener = open
-    with opener(path, "rb") as fh:
-        return parse_bytes(fh.read())
+    """Read a BAL file from disk, plain or gzip / bzip2 compressed (bal_io.py:229-241).
 
-
-def write_bal(problem: BaProblem, stream: IO[str]) -> None:
-    """Serialize losslessly (17 significant digits; bal_io.py:206-226)."""
-    stream.write(f"{problem.num_cameras} {problem.num_landmarks} {problem.num_observations}\n")
-    for c, l, m in zip(problem.camera_indices, problem.landmark_indices, problem.measurements):
-        stream.write(f"{c} {l} {m[0]:.17g} {m[1]:.17g}\n")
-    cams = problem.metric_cameras
-    if cams is None:
-        cams = np.zeros((problem.num_cameras, CAMERA_FIELDS))
-    for row in cams:
-        for v in row:
-            stream.write(f"{v:.17g}\n")
-    pts = problem.metric_points
-    if pts is None:
-        pts = np.zeros((problem.num_landmarks, POINT_FIELDS))
-    for row in pts:
-        for v in row:
-            stream.write(f"{v:.17g}\n")
+    The whole (decompressed) file is handed to the native multi-threaded parser.
+    """
+    raw = Path(path).read_bytes()
+    codec = next((name for magic, name in _CODECS if raw.startswith(magic)), None)
+    if codec is not None:
+        raw = __import__(codec).decompress(raw)
+    return parse_bytes(raw)
 
 
 def prune_underobserved(problem: BaProblem, min_cameras: int = 2) -> BaProblem:
@@ -126,23 +110,23 @@ def prune_underobserved(problem: BaProblem, min_cameras: int = 2) -> BaProblem:
                                 cam_seen.ctypes.data_as(u8), ctypes.byref(kept))
     if rc != 0:
         raise ValueError("observation indices out of range")
-    keep_lm = keep_lm.astype(bool)
-    cam_seen = cam_seen.astype(bool)
+    keep_lm = keep_lm.view(bool)
+    cam_seen = cam_seen.view(bool)
     if keep_lm.all() and cam_seen.all():
-        return problem
-    obs_keep = keep_lm[li]
-    lm_map = np.cumsum(keep_lm) - 1
-    cam_map = np.cumsum(cam_seen) - 1
+        return problem  # nothing to drop: the caller's object (bal_io.py:261-262)
+    n_cam, n_lm = int(np.count_nonzero(cam_seen)), int(np.count_nonzero(keep_lm))
+    # dense renumbering of the survivors: old id -> rank among the kept ids
+    new_cam = np.full(problem.num_cameras, -1, dtype=np.int64)
+    new_cam[cam_seen] = np.arange(n_cam)
+    new_lm = np.full(problem.num_landmarks, -1, dtype=np.int64)
+    new_lm[keep_lm] = np.arange(n_lm)
+    rows = np.flatnonzero(keep_lm[li])  # surviving observations, original order
     logger.info("pruned %d under-observed landmarks and %d empty cameras",
-                int((~keep_lm).sum()), int((~cam_seen).sum()))
-    return BaProblem(
-        num_cameras=int(cam_seen.sum()),
-        num_landmarks=int(keep_lm.sum()),
-        num_observations=int(kept.value),
-        camera_indices=cam_map[ci[obs_keep]],
-        landmark_indices=lm_map[li[obs_keep]],
-        measurements=problem.measurements[obs_keep],
-        metric_cameras=None if problem.metric_cameras is None
-        else problem.metric_cameras[cam_seen],
-        metric_points=None if problem.metric_points is None else problem.metric_points[keep_lm],
-    )
+                problem.num_landmarks - n_lm, problem.num_cameras - n_cam)
+
+    def subset(a, mask):
+        return None if a is None else a[mask]
+
+    return BaProblem(n_cam, n_lm, int(kept.value), new_cam[ci[rows]], new_lm[li[rows]],
+                     problem.measurements[rows], subset(problem.metric_cameras, cam_seen),
+                     subset(problem.metric_points, keep_lm))

@@ -63,6 +63,7 @@ struct pv_ctx {
 
   int64_t n_p = 0, n_l_global = 0, n_o_global = 0;
   int n_ls = 0, n_os = 0, n_tasks = 0;
+  size_t cpart_cap = 0;  // warp partials held by cpart (level-2 sums live after them)
   std::vector<int64_t> lm_gid;  // local -> global landmark id
   Coef coef{};
 
@@ -104,7 +105,8 @@ struct pv_ctx {
   // state and solve buffers (device)
   double *crec, *lrec, *lvr, *lbl, *ldl, *tlm, *tcam, *cs_x;
   double *lsys = nullptr, *tarr = nullptr, *sbuf = nullptr;
-  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *cpart, *ctmp, *scal;
+  double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *ctmp, *scal;
+  double* cpart = nullptr;
   int* flags;
   unsigned* ticket;
   PowerCtl* ctl;
@@ -121,7 +123,7 @@ struct pv_ctx {
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
   // reduced RHS reuse: -(b_p - W V+ b_l) depends on the linearization only when V+ is
   // undamped (POSE_ONLY), so a rejected step's next solve skips its camera pass
-  int64_t lin_id = 0, rhs_lin_id = -1;
+  int64_t lin_id = 0, rhs_lin_id = -1, damp_lin_id = -1;
   bool last_damp_both = true;
   int step_stage = 0;
 
@@ -155,10 +157,19 @@ struct pv_ctx {
   // deterministic sum of n (default n_tasks <= the buffer's capacity) warp partials
   void sum_partials(int n = -1) {
     if (n < 0) n = n_tasks;
+    if ((size_t)n > cpart_cap) throw PvError(PV_ECUDA, "partials exceed the cpart capacity");
     const int nb2 = std::max(1, std::min(256, (n + 4095) / 4096));
-    k_sum<<<nb2, 1024, 0, stream>>>(cpart, std::max(n, 1), cpart + n_tasks + 8);
-    k_sum<<<1, 1024, 0, stream>>>(cpart + n_tasks + 8, nb2, scal);
+    double* lvl2 = cpart + cpart_cap + 8;
+    k_sum<<<nb2, 1024, 0, stream>>>(cpart, std::max(n, 1), lvl2);
+    k_sum<<<1, 1024, 0, stream>>>(lvl2, nb2, scal);
     launched(2);
+  }
+  // cudaFuncSetAttribute is per device context: remember it per kernel and context
+  std::vector<const void*> attr_set;
+  void max_dyn_smem(const void* fn, int bytes) {
+    if (std::find(attr_set.begin(), attr_set.end(), fn) != attr_set.end()) return;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr_set.push_back(fn);
   }
 };
 
@@ -306,6 +317,18 @@ static void free_tracked(pv_ctx* c, T*& p, size_t bytes) {
   if (it != c->allocs.end()) c->allocs.erase(it);
   c->device_bytes -= bytes;
   p = nullptr;
+}
+
+// warp partials of the deterministic two-level sums: one per landmark task (k_cost,
+// k_resolve), per cost segment (k_cost_cs, <= n_tasks) or per landmark warp slot
+// (k_resolve_slots: blk_ktask[n_blk], which depends on the blocking), then the level-2 sums
+static void ensure_cpart(pv_ctx* c) {
+  const size_t ns = c->blk_ktask.empty() ? 0 : (size_t)c->blk_ktask[c->n_blk];
+  const size_t need = std::max<size_t>({(size_t)c->n_tasks, ns, 1});
+  if (c->cpart && need <= c->cpart_cap) return;
+  free_tracked(c, c->cpart, (c->cpart_cap + 8 + 256) * sizeof(double));
+  c->cpart = c->alloc<double>(need + 8 + 256);
+  c->cpart_cap = need;
 }
 
 // Work lists of k_cam_pipe (pv_pipe.cuh): for every landmark block and both passes,
@@ -563,6 +586,7 @@ static void build_blocks(pv_ctx* c) {
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
   build_pipe_items(c, seg);
   build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
+  if (c->cpart) ensure_cpart(c);   // re-blocking changes the number of warp slots
 }
 
 static void alloc_buffers(pv_ctx* c) {
@@ -588,7 +612,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->cyr = c->alloc<double>(np * 12);
   c->cUraw = c->alloc<double>(np * LINP);
   c->nrm = c->alloc<double>(np * 2);
-  c->cpart = c->alloc<double>((size_t)c->n_tasks + 8 + 256);  // warp partials + level 2
+  ensure_cpart(c);  // warp partials + level 2
   c->ctmp = c->alloc<double>(np * 12);
   c->scal = c->alloc<double>(8);
   c->flags = c->alloc<int>(F_COUNT);
@@ -652,11 +676,7 @@ static int op_linearize(pv_ctx* c) {
     c->launched();
   }
   c->lm_lin_fresh = false;
-  static bool lin_attr = false;
-  if (!lin_attr) {
-    CK(cudaFuncSetAttribute(k_lin_cam<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, LIN_SMEM));
-    lin_attr = true;
-  }
+  c->max_dyn_smem((const void*)k_lin_cam<S>, LIN_SMEM);
   k_lin_cam<S><<<(int)c->n_p, FT, LIN_SMEM, c->stream>>>(c->g, c->crec, c->cs_x, c->cUraw,
                                                          c->coef);
   c->launched(2);
@@ -683,7 +703,9 @@ template <int S>
 static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   const int D = S == 1 ? 12 : 11;
   c->last_damp_both = both != 0;
+  c->damp_lin_id = -1;
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_U, 0, 2 * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(c->flags + F_SINGULAR_M2, 0, sizeof(int), c->stream));
   k_damp_cam<<<blocks_for(c->n_p, 64), 64, 0, c->stream>>>((int)c->n_p, D, c->cU, lam, c->cUd,
                                                            c->cUi, c->flags);
   c->launched();
@@ -698,18 +720,27 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   int fl[F_COUNT];
   CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
+  if (fl[F_SINGULAR_U]) {
+    // a damped pose block that is not positive definite (lam = 0 and an unconstrained
+    // camera): np.linalg.inv (solvers.py:108-109) inverts it exactly by LU with partial
+    // pivoting, or raises LinAlgError on an exactly singular block
+    k_inv_lu<<<blocks_for(c->n_p, 32), 32, 0, c->stream>>>((int)c->n_p, D, c->cUd, c->cUi,
+                                                           c->flags);
+    c->launched();
+    c->check_launch();
+    c->allreduce_flags();
+    CK(cudaMemcpyAsync(fl, c->flags, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (fl[F_SINGULAR_M2]) throw PvError(PV_ESINGULAR, "Singular matrix");
+  }
+  c->damp_lin_id = c->lin_id;
   if (n_deg) *n_deg = fl[F_N_DEGEN];
 }
 
 template <int S, bool HC, int EP, bool HA>
 static void launch_cam_v(pv_ctx* c, const CamArgs& ca) {
   constexpr int smem = CAM_SMEM;
-  static bool attr_set = false;  // per template instantiation
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_cam<S, HC, EP, HA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            smem));
-    attr_set = true;
-  }
+  c->max_dyn_smem((const void*)k_cam<S, HC, EP, HA>, smem);
   CamArgs a = ca;
   a.wpc = c->wpc;
   const int cams_per_cta = 8 / c->wpc;
@@ -831,6 +862,22 @@ static void mark_rhs(pv_ctx* c) {
   c->rhs_lin_id = (S == 1 && !c->last_damp_both) ? c->lin_id : -1;
 }
 
+// K7: dl = -V+ (b_l + W^T x) (zero for degenerate blocks) and the trial landmarks, with
+// v = x (the pose update in cx), block by block so that each block's s stays in L2
+// (back_substitute, normal_eq.py:239-250)
+template <int S>
+static void back_substitute_dev(pv_ctx* c) {
+  k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
+  c->launched();
+  for (int b = 0; b < c->n_blk; ++b) {
+    CamArgs a = cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0);
+    a.disc_lo = b - 1;  // consumed by the previous block's back-substitution
+    launch_cam<S, false, EP_NONE, true>(c, a);
+    launch_lm_reduce<S, LR_BACKSUB>(c, b, b + 1, 0);
+  }
+  c->check_launch();
+}
+
 template <int S>
 static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* trunc) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
@@ -863,16 +910,7 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     }
   }
   c->check_launch();
-  // K7 back-substitution with v = x, block by block (s stays in L2)
-  k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
-  c->launched();
-  for (int b = 0; b < B; ++b) {
-    CamArgs a = cam_args(0, 0, 0, b, b + 1, 0, thr, 0);
-    a.disc_lo = b - 1;  // consumed by the previous block's back-substitution
-    launch_cam<S, false, EP_NONE, true>(c, a);
-    launch_lm_reduce<S, LR_BACKSUB>(c, b, b + 1, 0);
-  }
-  c->check_launch();
+  back_substitute_dev<S>(c);
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
@@ -898,6 +936,8 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   const int B = c->n_blk;
   const int wg = blocks_for((long long)np * 32, 256);  // one warp per camera
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_M, 0, 2 * sizeof(int), c->stream));
+  // a collapsed norm of an earlier trial must not leak into this solve (op_power does the same)
+  CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
   // K4: the reduced RHS (its U^-1 epilogue output is unused here)
   if (!rhs_reusable<S>(c)) {
     launch_lm_reduce<S, LR_RHS>(c, 0, c->n_blk, 0);
@@ -957,16 +997,7 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
     }
   }
   c->check_launch();
-  // K7 back-substitution with v = x
-  k_setv<S><<<blocks_for(np, 128), 128, 0, c->stream>>>((int)np, c->cx, c->ch, c->crec);
-  c->launched();
-  for (int b = 0; b < B; ++b) {
-    CamArgs a = cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0);
-    a.disc_lo = b - 1;
-    launch_cam<S, false, EP_NONE, true>(c, a);
-    launch_lm_reduce<S, LR_BACKSUB>(c, b, b + 1, 0);
-  }
-  c->check_launch();
+  back_substitute_dev<S>(c);
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
@@ -1211,8 +1242,6 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_CAM_PIPE:
       c->tune.cam_pipe = value ? 1 : 0;
       break;
-    case PV_OPT_GATHER_ASYNC:  // removed variant; accepted as a no-op (ABI stability)
-      break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
       c->block_bytes = value;
@@ -1319,7 +1348,8 @@ int pv_power_solve(pv_ctx* c, int max_order, double thr, int* order, double* tru
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
   if (max_order < 0 || !(thr >= 0.0)) throw PvError(PV_EINVAL, "power series settings");
-  if (c->lin_stage == 0) throw PvError(PV_EINVAL, "pv_power_solve before pv_linearize");
+  if (c->lin_stage == 0 || c->damp_lin_id != c->lin_id)
+    throw PvError(PV_EINVAL, "pv_power_solve needs pv_linearize + pv_damp first");
   int o = 0;
   double t = 0.0;
   STAGE_DISPATCH(c->lin_stage, op_power, c, max_order, thr, &o, &t);
@@ -1332,7 +1362,8 @@ int pv_pcg_solve(pv_ctx* c, int max_iterations, double tolerance, int* iteration
                  double* relative_residual, int* flag) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
-  if (c->lin_stage == 0) throw PvError(PV_EINVAL, "pv_linearize first");
+  if (c->lin_stage == 0 || c->damp_lin_id != c->lin_id)
+    throw PvError(PV_EINVAL, "pv_pcg_solve needs pv_linearize + pv_damp first");
   if (max_iterations < 0) throw PvError(PV_EINVAL, "max_iterations must be >= 0");
   int its = 0, fl = 0;
   double r = 0.0;
@@ -1375,6 +1406,27 @@ int pv_resolve_current(pv_ctx* c, int64_t* n_rd) {
   op_resolve_trial(c, nullptr, n_rd);
   op_accept(c, true);
   c->sync();
+  API_END(c)
+}
+
+int pv_back_substitute(pv_ctx* c, const double* dx) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  if (c->lin_stage == 0 || c->damp_lin_id != c->lin_id)
+    throw PvError(PV_EINVAL, "pv_back_substitute needs pv_linearize + pv_damp first");
+  if (!dx) throw PvError(PV_EINVAL, "null pose update");
+  const int S = c->lin_stage, D = S == 1 ? 12 : 11;
+  std::vector<double> h((size_t)c->n_p * 12, 0.0);
+  for (int64_t i = 0; i < c->n_p; ++i)
+    for (int q = 0; q < D; ++q) h[i * 12 + q] = dx[i * D + q];
+  CK(cudaMemcpyAsync(c->cx, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
+  if (S == 1)
+    back_substitute_dev<1>(c);
+  else
+    back_substitute_dev<2>(c);
+  c->sync();
+  c->step_stage = S;
   API_END(c)
 }
 
@@ -1428,7 +1480,7 @@ int pv_schur_apply(pv_ctx* c, int stage, const double* v, double* out) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
   if (c->lin_stage != stage) throw PvError(PV_EINVAL, "no linearization of that stage");
-  if (!c->vp_cached && c->lsys == nullptr) throw PvError(PV_EINVAL, "pv_damp first");
+  if (c->damp_lin_id != c->lin_id) throw PvError(PV_EINVAL, "pv_damp first");
   STAGE_DISPATCH(stage, op_schur_apply, c, v, out);
   API_END(c)
 }

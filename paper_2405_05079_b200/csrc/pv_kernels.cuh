@@ -34,7 +34,7 @@ struct Tune {
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
   int discard_s;   // drop consumed s lines from L2 (no write-back)
-  int reserved7;     // (PV_OPT_GATHER_ASYNC: a removed asynchronous-gather k_cam variant)
+  int reserved7;     // (option 7: a removed camera-kernel variant)
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v

@@ -29,7 +29,7 @@ import numpy as np
 from . import _lib
 from .types import (BOTH, JOINT, POSE_ONLY, STAGE1, STAGE2, VARPRO, BaProblem,
                     ConvergenceTrace, NumericFailureError, PoseConfig, ProjectiveState,
-                    SolverConfig, StepReport, TraceRecord, solver_label)
+                    UNIT_TOL, SolverConfig, StepReport, TraceRecord, solver_label)
 
 
 class DeviceProblem:
@@ -166,6 +166,12 @@ class DeviceProblem:
         self._call("pv_resolve_current", ctypes.byref(n))
         return n.value
 
+    def back_substitute(self, dx: np.ndarray) -> None:
+        """Device back-substitution of a given pose update on the damped system
+        (normal_eq.py:239-250); the result becomes the device step (``step``, ``trial``)."""
+        dx = np.ascontiguousarray(dx, dtype=np.float64)
+        self._call("pv_back_substitute", _lib.dptr(dx))
+
     def step(self, stage: int) -> tuple[np.ndarray, np.ndarray]:
         d = 12 if stage == STAGE1 else 11
         dx = np.zeros(self.n_p * d)
@@ -196,6 +202,43 @@ class DeviceProblem:
         out = np.zeros(sizes[which])
         self._call("pv_debug_get", int(which), _lib.dptr(out))
         return out
+
+
+def _check_unit(state: ProjectiveState) -> None:
+    """The tangent bases need unit vectors (riemannian.py:46-48, UNIT_TOL = riemannian.py:26).
+
+    The device derives the Householder bases from the state itself, so this is the
+    reference's check on the same vectors: every camera 12-vector, then every landmark.
+    """
+    for v in (state.cameras.reshape(len(state.cameras), 12), state.landmarks):
+        if len(v) and np.abs(np.linalg.norm(v, axis=-1) - 1.0).max() > UNIT_TOL:
+            raise ValueError("tangent basis requires unit vectors; retract first")
+
+
+def _householder_bases(v: np.ndarray) -> np.ndarray:
+    """The deterministic Householder complement bases (riemannian.py:37-56), (..., n, n-1)."""
+    n = v.shape[-1]
+    sigma = np.where(v[..., 0] >= 0, 1.0, -1.0)
+    u = np.array(v, dtype=np.float64, copy=True)
+    u[..., 0] += sigma
+    u /= np.linalg.norm(u, axis=-1, keepdims=True)
+    basis = -2.0 * u[..., :, None] * u[..., None, 1:]
+    idx = np.arange(n - 1)
+    basis[..., idx + 1, idx] += 1.0
+    return basis
+
+
+def _check_bases(state: ProjectiveState, bases) -> None:
+    """Bases passed to ``riemannian_step`` must be the state's own Householder bases: the
+    device applies those implicitly (h vectors, never stored) and cannot take others."""
+    cams = state.cameras.reshape(len(state.cameras), 12)
+    for given, v, name in ((bases.camera_bases, cams, "camera"),
+                           (bases.landmark_bases, state.landmarks, "landmark")):
+        given = np.asarray(given, dtype=np.float64)
+        want = _householder_bases(v)
+        if given.shape != want.shape or not np.allclose(given, want, rtol=0.0, atol=1e-12):
+            raise ValueError(f"{name} bases differ from the Householder bases of the state "
+                             "(riemannian.py:37-56), the only bases the device path applies")
 
 
 def _default_device() -> int:
@@ -301,6 +344,16 @@ def power_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
     return StepReport(dx, dl, order, order, trunc)
 
 
+def back_substitute(system: SchurSystem, pose_update: np.ndarray) -> np.ndarray:
+    """normal_eq.py:239-250 on a device system: -V^+(b_l + W^T dx_p), zero for degenerate
+    landmark blocks; (n_landmarks * 3,) like the reference."""
+    pose_update = np.asarray(pose_update, dtype=np.float64).ravel()
+    if pose_update.size != system.pose_dim:
+        raise ValueError("pose update does not match the system")
+    system.dp.back_substitute(pose_update)
+    return system.dp.step(system.stage)[1]
+
+
 def pcg_schur_solve(system: SchurSystem, config: SolverConfig) -> StepReport:
     """solvers.py:153-187 on a device system (block-Jacobi PCG, exact diagonal blocks)."""
     its, rel_res, flag = system.dp.pcg_solve(config.max_inner_iterations, config.pcg_tolerance)
@@ -363,11 +416,16 @@ def riemannian_step(problem: BaProblem, state: ProjectiveState, config: SolverCo
                     ) -> StepReport:
     """riemannian.py:125-138: tangent-space reduced solve (11 per camera, 3 per landmark).
 
-    ``bases`` is accepted for signature compatibility; the device derives the
-    same Householder bases (riemannian.py:37-56) from ``state``.
+    The device derives the Householder bases (riemannian.py:37-56) from ``state``; as in
+    the reference, a state off the unit spheres raises ``ValueError`` when no bases are
+    given, and given ``bases`` must be those of ``state`` (checked on the host).
     """
     if lam is None:
         lam = config.initial_lambda
+    if bases is None:
+        _check_unit(state)
+    else:
+        _check_bases(state, bases)
     system = assemble_system(problem, state, STAGE2, lam, BOTH, config.pose, dp=dp)
     return solve_reduced(system, config)
 
@@ -406,6 +464,10 @@ def lm_minimize(problem: BaProblem, state: ProjectiveState, stage: int, config: 
     lam = config.initial_lambda
     linearized = False
     for it in range(1, config.max_outer_iterations + 1):
+        if stage == STAGE2 and it == 1:
+            # state_tangent_bases of the start (solvers.py:358-359): later states are
+            # retracted trials, unit by construction
+            _check_unit(state)
         if not linearized:
             dp.linearize(stage)  # FloatingPointError on a degenerate stage-2 point
             linearized = True

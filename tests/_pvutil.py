@@ -23,3 +23,23 @@ def problem_from(z):
     from paper_2405_05079_b200.types import BaProblem
     return BaProblem(int(z["n_cameras"]), int(z["n_landmarks"]), len(z["cam_idx"]),
                      z["cam_idx"].astype(np.int64), z["lm_idx"].astype(np.int64), z["meas"])
+
+
+REF_INSTALL = ROOT / "baseline" / "_ref"
+
+
+def reference_stratba():
+    """The UNMODIFIED reference package installed under baseline/_ref (git-ignored; it
+    travels to the GPU box with the working tree).  Used only as the caller whose plug
+    point is switched to the device path, never as the thing measured."""
+    import importlib
+    import sys
+    if not (REF_INSTALL / "stratba" / "__init__.py").exists():
+        import pytest
+        pytest.skip("reference not installed under baseline/_ref (DESIGN.md section 7)")
+    if str(REF_INSTALL) not in sys.path:
+        sys.path.insert(0, str(REF_INSTALL))
+    mod = importlib.import_module("stratba")
+    for sub in ("solvers", "pipeline", "bal_io", "evaluation", "riemannian", "objective"):
+        importlib.import_module("stratba." + sub)
+    return mod

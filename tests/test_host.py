@@ -128,3 +128,66 @@ def test_retract_and_lift():
     np.testing.assert_allclose(np.linalg.norm(r.landmarks, axis=1), 1.0)
     with pytest.raises(ValueError):
         pv.retract(pv.ProjectiveState(np.zeros((1, 3, 4)), np.ones((1, 4))))
+
+
+def test_integration_switch_rebinds_and_restores():
+    """integration.enable rebinds the reference's lm_minimize (solvers + pipeline namespaces,
+    pipeline.py:18) and optionally random_init; disable restores them (no GPU call)."""
+    from _pvutil import reference_stratba
+    from paper_2405_05079_b200 import integration, solver
+    stratba = reference_stratba()
+    ref_lm, ref_init = stratba.solvers.lm_minimize, stratba.pipeline.random_init
+    integration.enable(stratba, random_init=True)
+    try:
+        assert stratba.pipeline.lm_minimize is stratba.solvers.lm_minimize is not ref_lm
+        assert stratba.pipeline.random_init is solver.random_init
+        assert stratba.bal_io.random_init is solver.random_init
+    finally:
+        integration.disable()
+    assert stratba.solvers.lm_minimize is ref_lm and stratba.pipeline.lm_minimize is ref_lm
+    assert stratba.pipeline.random_init is ref_init
+
+
+def test_stage2_rejects_non_unit_state_before_any_device_work():
+    """riemannian.py:46-48: the tangent basis needs unit vectors.  The check runs on the
+    host before the device is touched, with the reference's message (tests/golden/degen.npz
+    holds the reference's own exception text)."""
+    from _pvutil import golden
+    from paper_2405_05079_b200 import solver
+    from paper_2405_05079_b200.types import ProjectiveState
+    z = golden("degen.npz")
+    st = ProjectiveState(z["cams"], z["lms"])
+    with pytest.raises(ValueError) as ei:
+        solver._check_unit(st)
+    assert str(ei.value) == str(z["nonunit_message"])
+    cams = st.cameras.reshape(len(st.cameras), 12)
+    unit = ProjectiveState((cams / np.linalg.norm(cams, axis=1)[:, None]).reshape(-1, 3, 4),
+                           st.landmarks / np.linalg.norm(st.landmarks, axis=1)[:, None])
+    solver._check_unit(unit)
+    bad = np.array(unit.landmarks)
+    bad[3] *= 1.0 + 2e-9  # beyond UNIT_TOL = 1e-9 (riemannian.py:26)
+    with pytest.raises(ValueError):
+        solver._check_unit(ProjectiveState(unit.cameras, bad))
+
+
+def test_householder_bases_match_reference_convention():
+    """riemannian_step's bases argument is validated against the Householder construction
+    (riemannian.py:37-56) the device applies implicitly."""
+    from _pvutil import reference_stratba
+    from paper_2405_05079_b200 import solver
+    from paper_2405_05079_b200.types import ProjectiveState
+    stratba = reference_stratba()
+    rng = np.random.default_rng(4)
+    cams = rng.standard_normal((5, 12))
+    cams[0, 0] = -abs(cams[0, 0])
+    cams /= np.linalg.norm(cams, axis=1)[:, None]
+    lms = rng.standard_normal((9, 4))
+    lms /= np.linalg.norm(lms, axis=1)[:, None]
+    st = ProjectiveState(cams.reshape(5, 3, 4), lms)
+    ref = stratba.riemannian.state_tangent_bases(st)
+    np.testing.assert_allclose(solver._householder_bases(cams), ref.camera_bases, atol=1e-15)
+    solver._check_bases(st, ref)
+    other = stratba.riemannian.TangentBasis(ref.camera_bases[:, :, ::-1].copy(),
+                                            ref.landmark_bases)
+    with pytest.raises(ValueError):
+        solver._check_bases(st, other)
