@@ -6,16 +6,25 @@ on; it fits one B200): the seeded 13,682-camera / 4,456,117-landmark /
 series, <= 30 terms, threshold 0.01), random N(0,1) start.
 
 * a "step" = one full stage-1 LM iteration (linearize, damp, power series,
-  back-substitution, trial, cost, accept + closed-form landmark re-solve)
-  continuing an LM run; ``value`` = n_obs x iterations/s (obs/s), inputs
-  resident in HBM.
-* ``spmv`` = the S'.v term alone (the power-series unit of work).
-* ``roofline`` = the dominant term kernel, algorithmic bytes / mean launch
-  time from CUDA events inside this run.
-* ``e2e`` = the public ``lm_minimize`` call with host state in / out
-  (one iteration per call), i.e. host<->device copies inside the timing.
-* ``--impl reference`` times the CPU oracle port (oracle/povar_oracle.py, the
-  NumPy restatement of the reference) on a landmark-subsampled slice.
+  back-substitution, trial, cost, accept + closed-form landmark re-solve).
+  ``value`` = n_obs x iterations/s (obs/s) over LM iterations 1..K from the
+  random start (north_star's "first 20"), inputs resident in HBM: the W warm-up
+  iterations run first and the state is then reset to the start, so ``value``
+  and ``e2e`` time the SAME iterations (same power orders, printed for both).
+* ``e2e`` = the public ``lm_minimize(max_outer_iterations=K)`` call from a pinned
+  host state to a host result (state upload, initial cost, K iterations, state
+  download); ``setup_s`` = ``DeviceProblem`` creation (graph sort + upload), the
+  one-off cost a first call pays, reported beside it.
+* ``spmv`` = the S'.v term alone (the power-series unit of work); ``breakdown``
+  = the LM iteration split by operation (CUDA events between the calls).
+* ``roofline`` = the dominant term kernel: DRAM-compulsory bytes of the declared
+  layout (the L2-resident partials s and vectors t are
+  excluded and reported separately) / its time, every block's launch timed with
+  CUDA events; ``frac_traffic`` the same with the ncu-measured DRAM bytes.
+* ``cpu_baseline`` / ``--impl reference``: the reference's own CPU path (the
+  unmodified ``stratba`` installed under baseline/_ref; the NumPy oracle port if
+  that install is absent) on a landmark-subsampled slice, at 1 and all host
+  threads, with the host recorded.
 
 Multi-GPU: ``torchrun --nproc-per-node N bench.py --gpus N``: landmarks are
 sharded across ranks (equal observation counts), cameras replicated, one NCCL
@@ -106,22 +115,24 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def term_bytes(n_p, n_l, n_o, stage=1):
-    """Algorithmic bytes of one power-series term per kernel.
+def term_bytes(n_p, n_l, n_o, stage=1, x_bytes=32):
+    """Bytes of one power-series term per kernel group.
 
-    Every array element a kernel must touch, counted once per pass.  k_cam
-    (summed over the landmark blocks) streams the camera-sorted x (32), m (16)
-    and one id (4) twice -- once for W t, once for W^T v -- scatters s (32) and
-    reads each landmark's t once (32 per landmark), plus per camera P, U^-1 and
-    the small vectors (~1.6 KB).  k_lm_reduce reads s (32 per observation) and
-    per landmark its work-slot entry (16), V+ (2 x 32 B sectors), x (stage 2) and
-    writes t (32).  s and t are sized per block to stay in the persisting L2,
-    so the DRAM-compulsory part is the streams + per-landmark data.
+    ``dram``: what the declared layout must move between HBM and the SMs per term.
+    The camera passes stream the camera-sorted x (``x_bytes``), m (16) and one int32
+    id (4) twice -- once for W t, once for W^T v -- plus per camera the 192-byte record
+    per pass and y (96); the landmark reduces read each landmark's V+ record (64) and
+    its work-slot entry (16; stage 2 also x, 32).  ``l2``: the transposes that the
+    landmark blocking keeps in the persisting L2 by design -- the partials s (written
+    and read, 32 per observation) and the vectors t (written per landmark, gathered per
+    observation).  ``r1_term``: the reference's own layout (W stored, SURVEY section
+    8(d)), for the north_star's roofline figure.
     """
-    lmr = 32 * n_o + (112 if stage == 1 else 144) * n_l
-    cam = 136 * n_o + 32 * n_l + 1600 * n_p
+    cam = 2 * (x_bytes + 16 + 4) * n_o + (2 * 192 + 96) * n_p
+    lmr = (80 if stage == 1 else 112) * n_l
+    l2 = {"cam": 32 * n_o + 32 * n_o, "lm_reduce": 32 * n_o + 32 * n_l}
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
-    return {"lm_reduce": lmr, "cam": cam, "r1_term": r1}
+    return {"dram": {"cam": cam, "lm_reduce": lmr}, "l2": l2, "r1_term": r1}
 
 
 def traffic_from_profile(kernel, n_o):
@@ -136,52 +147,103 @@ def traffic_from_profile(kernel, n_o):
     return None
 
 
-def cpu_port_lm(fraction, iters=2, seed=0):
-    """Time the oracle port (NumPy restatement of the reference) on a slice."""
-    from oracle import povar_oracle as O
+def reference_package():
+    """The unmodified reference (``stratba``) installed under baseline/_ref, or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.exists(os.path.join(path, "stratba", "__init__.py")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import stratba
+    import stratba.solvers  # noqa: F401
+    return stratba
+
+
+def host_record():
+    import numpy as np
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")),
+                         "")
+    except OSError:
+        pass
+    blas = {}
+    try:
+        b = np.show_config(mode="dicts")["Build Dependencies"]["blas"]
+        blas = {"name": b.get("name"), "version": b.get("version")}
+    except Exception:
+        pass
+    return {"cpu": model, "nproc": len(os.sched_getaffinity(0)), "numpy": np.__version__,
+            "blas": blas}
+
+
+def cpu_lm(fraction, iters, threads, warm=0, seed=0):
+    """Time ``iters`` stage-1 LM iterations 1..iters from the random start on a landmark
+    subsample of vlarge with ``threads`` BLAS/OpenMP threads: the reference's own
+    ``lm_minimize`` (solvers.py:318-393) when installed, else the NumPy oracle port."""
+    from threadpoolctl import threadpool_limits
+
     from paper_2405_05079_b200 import synth
     problem, _ = synth.make_problem(CONFIG, seed, landmark_fraction=fraction)
     state = synth.random_state(problem, 1)
-    g = O.graph_of(problem)
-    cams, lms = np.array(state.cameras), np.array(state.landmarks)
-    O.lm_minimize(g, cams, lms, 1, max_iterations=1, max_order=30, ftol=1e-300)  # warm
-    t = time.perf_counter()
-    log = O.lm_minimize(g, cams, lms, 1, max_iterations=iters, max_order=30, ftol=1e-300)
-    dt = (time.perf_counter() - t) / max(1, len(log.decisions))
-    return problem.num_observations / dt, dt, problem
+    stratba = reference_package()
+    with threadpool_limits(threads):
+        if stratba is not None:
+            rp = stratba.BaProblem(problem.num_cameras, problem.num_landmarks,
+                                   problem.num_observations, problem.camera_indices,
+                                   problem.landmark_indices, problem.measurements)
+            st = stratba.ProjectiveState(state.cameras, state.landmarks)
+
+            def run(k):
+                cfg = stratba.SolverConfig(max_outer_iterations=k, max_power_order=30,
+                                           function_tolerance=1e-300)
+                t = time.perf_counter()
+                _, tr = stratba.solvers.lm_minimize(rp, st, 1, cfg)
+                return time.perf_counter() - t, len(tr.records) - 1
+            kind = "reference"
+        else:
+            from oracle import povar_oracle as O
+            g = O.graph_of(problem)
+            cams, lms = np.array(state.cameras), np.array(state.landmarks)
+
+            def run(k):
+                t = time.perf_counter()
+                log = O.lm_minimize(g, cams, lms, 1, max_iterations=k, max_order=30,
+                                    ftol=1e-300)
+                return time.perf_counter() - t, len(log.decisions)
+            kind = "port"
+        if warm:
+            run(warm)
+        dt, n_it = run(iters)
+    return {"obs_per_s": problem.num_observations * n_it / dt, "s_per_iter": dt / n_it,
+            "iterations": n_it, "threads": threads, "kind": kind,
+            "n_obs": problem.num_observations}, problem
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     fr = CPU_SAMPLE_FRACTION
-    from oracle import povar_oracle as O
-    from paper_2405_05079_b200 import synth
-    problem, _ = synth.make_problem(CONFIG, 0, landmark_fraction=fr)
-    state = synth.random_state(problem, 1)
-    g = O.graph_of(problem)
-    cams, lms = np.array(state.cameras), np.array(state.landmarks)
-    # warmup + timed LM iterations of the NumPy port, continuing one LM run
-    log = O.lm_minimize(g, cams, lms, 1, max_iterations=max(1, args.warmup), max_order=30,
-                        ftol=1e-300)
-    cams, lms = log.cams, log.lms
-    t = time.perf_counter()
-    log = O.lm_minimize(g, cams, lms, 1, max_iterations=args.steps, max_order=30, ftol=1e-300)
-    dt = time.perf_counter() - t
-    n_it = len(log.decisions)
-    value = problem.num_observations * n_it / dt
+    nthr = len(os.sched_getaffinity(0))
+    r, problem = cpu_lm(fr, args.steps, nthr, warm=max(1, args.warmup))
+    value = r["obs_per_s"]
+    what = ("stratba.lm_minimize (baseline/_ref, unmodified reference)" if r["kind"] == "reference"
+            else "NumPy oracle port (oracle/povar_oracle.py)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "obs/s",
-            "n_gpus": world, "steps": n_it, "warmup": args.warmup,
-            "ms_per_step": 1e3 * dt / n_it, "higher_is_better": True, "scaling": "strong",
+            "n_gpus": world, "steps": r["iterations"], "warmup": args.warmup,
+            "ms_per_step": 1e3 * r["s_per_iter"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE vlarge generator, landmark-subsampled)",
-            "config": {"workload": "vlarge stage-1 PoVar LM iteration (CPU oracle port)",
+            "config": {"workload": f"vlarge stage-1 PoVar LM iterations 1..K, {what}",
                        "landmark_fraction": fr, "n_cameras": problem.num_cameras,
                        "n_landmarks": problem.num_landmarks,
                        "n_obs": problem.num_observations, "max_power_order": 30},
-            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": 1, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": nthr, "kind": r["kind"],
                              "sample": f"{fr:.0%} of vlarge landmarks "
-                                       f"({problem.num_observations} obs), {n_it} LM iterations"},
+                                       f"({problem.num_observations} obs), LM iterations "
+                                       f"1..{r['iterations']} from the random start, {what}",
+                             "host": host_record()},
             "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -190,7 +252,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=CONFIG)
@@ -222,8 +284,11 @@ def main():
     n_p, n_l, n_o = problem.num_cameras, problem.num_landmarks, problem.num_observations
     plan = shard.plan_shards(problem, world)
     nccl_id = shard.broadcast_nccl_id(rank, world) if world > 1 else None
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     dp = pv.DeviceProblem(problem, 0.1, device=local, rank=rank, world=world, nccl_id=nccl_id,
                           lm_range=plan[rank])
+    setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.ExternalStream(dp.stream_handle, device=local)
     scfg = pv.SolverConfig(max_outer_iterations=1, max_power_order=cfg.max_power_order,
                            function_tolerance=1e-300)
@@ -239,55 +304,79 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- LM iterations (value) -------------------------------------------------
-    dp.set_state(state0)
-    f = dp.cost(1)
-    lam = scfg.initial_lambda
-    orders = []
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
 
-    linearized = [False]
+    # ---- LM iterations 1..K from the random start (value) --------------------------
+    run = {}
+    ops = ("linearize", "damp", "power_solve", "trial_cost", "accept_resolve")
 
-    def lm_iteration():
+    def start_run():
+        dp.set_state(state0)
+        run.update(f=dp.cost(1), lam=scfg.initial_lambda, linearized=False, orders=[],
+                   marks=[])
+
+    def lm_iteration(timed=False):
         # solver.lm_minimize's iteration: a rejected step leaves the state unchanged, so its
         # linearization (and, POSE_ONLY, the reduced RHS) is reused
-        nonlocal f, lam
-        if not linearized[0]:
+        m = [ev()] if timed else None
+        if not run["linearized"]:
             dp.linearize(1)
-            linearized[0] = True
-        dp.damp(lam, False)
+            run["linearized"] = True
+        if timed:
+            m.append(ev())
+        dp.damp(run["lam"], False)
+        if timed:
+            m.append(ev())
         order, _ = dp.power_solve(scfg.max_power_order, scfg.power_threshold)
-        orders.append(order)
+        run["orders"].append(order)
+        if timed:
+            m.append(ev())
         ok = dp.trial(1)
         ft = dp.cost(1, trial=True) if ok else math.inf
-        if ft < f:
-            f, _ = dp.accept(1, resolve=True)
-            linearized[0] = False
-            lam = max(scfg.lambda_min, lam * scfg.lambda_decrease)
+        if timed:
+            m.append(ev())
+        if ft < run["f"]:
+            run["f"], _ = dp.accept(1, resolve=True)
+            run["linearized"] = False
+            run["lam"] = max(scfg.lambda_min, run["lam"] * scfg.lambda_decrease)
         else:
-            lam = min(scfg.lambda_max, lam * scfg.lambda_increase)
+            run["lam"] = min(scfg.lambda_max, run["lam"] * scfg.lambda_increase)
+        if timed:
+            m.append(ev())
+            run["marks"].append(m)
 
+    start_run()
     for _ in range(args.warmup):
         lm_iteration()
-    orders.clear()
+    start_run()  # iterations 1..K, exactly those e2e times
     launches0 = dp.info()["launches"]
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        e0.record(stream)
+        e0 = ev()
         for _ in range(args.steps):
-            lm_iteration()
-        e1.record(stream)
+            lm_iteration(timed=True)
+        e1 = ev()
         torch.cuda.synchronize()
     barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     launches = dp.info()["launches"] - launches0
     ms_step = ms_total / args.steps
     value = n_o * args.steps / (ms_total * 1e-3)
+    orders = list(run["orders"])
+    accepts = []
+    breakdown = {k: 0.0 for k in ops}
+    for m in run["marks"]:
+        for k, a, b in zip(ops, m, m[1:]):
+            breakdown[k] += a.elapsed_time(b) / args.steps
+    breakdown = {k: round(max_over_ranks(v), 4) for k, v in breakdown.items()}
 
-    # ---- S'.v terms and per-kernel roofline ------------------------------------
+    # ---- S'.v terms and per-kernel roofline (at the state after iteration K) ---------
     dp.linearize(1)
-    dp.damp(lam, False)
+    dp.damp(run["lam"], False)
     dp.power_solve(1, 0.0)
     dp.bench_terms(1, 3)
     barrier()
@@ -295,49 +384,60 @@ def main():
     kt = {k: max_over_ranks(v) for k, v in kt.items()}
     peak, peak_src = _peaks()
     loc = dp.info()
-    tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], 1)
-    kern = {}
     # one warp per camera: the persistent TMA-pipelined camera kernel runs the blocks
     cam_name = "k_cam_pipe" if loc["warps_per_cam"] == 1 else "k_cam"
-    for name, key, tkey in (("k_lm_reduce", "lm_reduce", "phase1_ms"),
-                            (cam_name, "cam", "phase2_ms")):
-        ms = kt[tkey]
-        gbs = tb[key] / (ms * 1e-3) / 1e9
-        kern[name] = {"ms": ms, "algorithmic_bytes": tb[key], "achieved_gbs": gbs,
-                      "frac": gbs / peak}
+
+    def term_report(kt, stage):
+        tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], stage,
+                        x_bytes=loc.get("x_bytes") or 32)
+        kern = {}
+        for name, key, tkey in (("k_lm_reduce", "lm_reduce", "lm_reduce_ms"),
+                                (cam_name, "cam", "cam_ms")):
+            ms = kt[tkey]
+            gbs = tb["dram"][key] / (ms * 1e-3) / 1e9
+            kern[name] = {"ms": ms, "dram_bytes": tb["dram"][key], "l2_bytes": tb["l2"][key],
+                          "achieved_gbs": gbs, "frac": gbs / peak}
+        term_ms = kt["term_ms"]
+        dram = sum(tb["dram"].values())
+        return {"ms_per_term": term_ms, "terms_per_s": 1e3 / term_ms,
+                "obs_per_s": n_o / (term_ms * 1e-3),
+                "dram_bytes_per_term": dram,
+                "dram_frac": dram / (term_ms * 1e-3) / 1e9 / peak,
+                "r1_equivalent_gbs": tb["r1_term"] * world / (term_ms * 1e-3) / 1e9,
+                "r1_equivalent_frac_of_8tbs": tb["r1_term"] * world / (term_ms * 1e-3) / 8e12,
+                "kernels": kern, "blocks": int(kt["blocks"])}
+
+    spmv = term_report(kt, 1)
+    kern = spmv["kernels"]
     dom = max(kern, key=lambda k: kern[k]["ms"])
-    term_ms = kt["term_ms"]
-    spmv = {"ms_per_term": term_ms, "terms_per_s": 1e3 / term_ms,
-            "obs_per_s": n_o / (term_ms * 1e-3),
-            "r1_equivalent_gbs": tb["r1_term"] * world / (term_ms * 1e-3) / 1e9,
-            "r1_equivalent_frac": tb["r1_term"] * world / (term_ms * 1e-3) / 1e9 / peak,
-            "r1_equivalent_frac_of_8tbs": tb["r1_term"] * world / (term_ms * 1e-3) / 8e12,
-            "kernels": kern}
+    traffic = traffic_from_profile(dom, n_o)
     roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak,
-                "unit": "GB/s", "frac": kern[dom]["frac"],
-                "traffic": traffic_from_profile(dom, n_o), "kernel": dom,
-                "peak_source": peak_src,
-                "note": "achieved/traffic per term (summed over the landmark-block launches)"}
+                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
+                "frac_traffic": (traffic / (kern[dom]["ms"] * 1e-3) / 1e9 / peak
+                                 if traffic else None),
+                "kernel": dom, "peak_source": peak_src,
+                "note": "per power-series term, summed over the landmark-block launches: "
+                        "achieved = DRAM-compulsory bytes of the layout / summed launch time "
+                        "(CUDA events around every launch); traffic = ncu dram bytes"}
+    non_term_ms = ms_step - float(np.mean(orders)) * spmv["ms_per_term"]
 
     # ---- PCG inner solver ("iterative", solvers.py:153-187) on the same system -----
     pcg = None
     if not args.no_pcg:
         dp.linearize(1)
-        dp.damp(lam, False)
+        dp.damp(run["lam"], False)
         dp.pcg_solve(2, 1e-300)  # warm
         tms = {}
         for n_it in (1, 21):  # tolerance 0 -> exactly n_it iterations
             barrier()
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            its, _, _ = dp.pcg_solve(n_it, 1e-300)
-            b.record(stream)
+            a = ev()
+            dp.pcg_solve(n_it, 1e-300)
+            b = ev()
             torch.cuda.synchronize()
             tms[n_it] = max_over_ranks(a.elapsed_time(b))
-        per_it = (tms[21] - tms[1]) / 20
-        pcg = {"ms_per_iteration": per_it, "ms_setup_plus_one_iteration": tms[1],
-               "ms_21_iterations": tms[21],
+        pcg = {"ms_per_iteration": (tms[21] - tms[1]) / 20,
+               "ms_setup_plus_one_iteration": tms[1], "ms_21_iterations": tms[21],
                "note": "RHS + exact Schur block diagonal + its inverse + back-substitution are "
                        "the setup; one iteration = one blocked S'.p term + 3 vector kernels"}
 
@@ -348,76 +448,96 @@ def main():
             s1 = dp.get_state()
             lifted = pv.lift_stage1_to_stage2(s1)
             dp.set_state(lifted)
-            f2 = dp.cost(2)
-            if math.isfinite(f2):
-                lam2 = scfg.initial_lambda
-
+            st2 = {"f": dp.cost(2), "lam": scfg.initial_lambda, "orders": []}
+            if math.isfinite(st2["f"]):
                 def it2():
-                    nonlocal f2, lam2
                     dp.linearize(2)
-                    dp.damp(lam2, True)
-                    dp.power_solve(scfg.max_power_order, scfg.power_threshold)
+                    dp.damp(st2["lam"], True)
+                    o, _ = dp.power_solve(scfg.max_power_order, scfg.power_threshold)
+                    st2["orders"].append(o)
                     ok = dp.trial(2)
                     ft = dp.cost(2, trial=True) if ok else math.inf
-                    if ft < f2:
+                    if ft < st2["f"]:
                         dp.accept(2, resolve=False)
-                        f2 = ft
-                        lam2 = max(scfg.lambda_min, lam2 * scfg.lambda_decrease)
+                        st2["f"] = ft
+                        st2["lam"] = max(scfg.lambda_min, st2["lam"] * scfg.lambda_decrease)
                     else:
-                        lam2 = min(scfg.lambda_max, lam2 * scfg.lambda_increase)
+                        st2["lam"] = min(scfg.lambda_max, st2["lam"] * scfg.lambda_increase)
                 it2()
+                st2["orders"].clear()
                 barrier()
                 torch.cuda.synchronize()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 n2 = max(3, args.steps // 2)
-                a.record(stream)
+                a = ev()
                 for _ in range(n2):
                     it2()
-                b.record(stream)
+                b = ev()
                 torch.cuda.synchronize()
                 ms2 = max_over_ranks(a.elapsed_time(b)) / n2
                 dp.linearize(2)
-                dp.damp(lam2, True)
-                kt2 = dp.bench_terms(2, 10)
-                stage2 = {"ms_per_iter": ms2, "obs_per_s": n_o / (ms2 * 1e-3),
-                          "ms_per_term": max_over_ranks(kt2["term_ms"])}
+                dp.damp(st2["lam"], True)
+                kt2 = {k: max_over_ranks(v) for k, v in dp.bench_terms(2, 10).items()}
+                t2 = term_report(kt2, 2)
+                k2 = t2["kernels"]
+                d2 = max(k2, key=lambda k: k2[k]["ms"])
+                stage2 = {"ms_per_iter": ms2, "obs_per_s": n_o / (ms2 * 1e-3), "iterations": n2,
+                          "mean_power_order": float(np.mean(st2["orders"])),
+                          "ms_per_term": t2["ms_per_term"], "spmv": t2,
+                          "roofline": {"bound": "hbm", "kernel": d2,
+                                       "achieved": k2[d2]["achieved_gbs"], "peak": peak,
+                                       "unit": "GB/s", "frac": k2[d2]["frac"]}}
         except Exception as e:  # report, do not fail the stage-1 line
             stage2 = {"error": f"{type(e).__name__}: {e}"}
 
-    # ---- e2e through the public API: one lm_minimize call of K iterations from a host
-    # state in pinned memory to a host result (upload, K iterations, download, trace)
+    # ---- e2e through the public API: one lm_minimize call of K iterations from the
+    # random start in pinned host memory to a host result -- the iterations value timed
     e2e = None
     if not args.no_e2e:
         cfgK = pv.SolverConfig(max_outer_iterations=args.steps,
                                max_power_order=cfg.max_power_order, function_tolerance=1e-300)
-        src = dp.get_state() if stage2 is None else state0
-        pin_c = torch.empty(src.cameras.shape, dtype=torch.float64, pin_memory=True).numpy()
-        pin_l = torch.empty(src.landmarks.shape, dtype=torch.float64, pin_memory=True).numpy()
-        pin_c[...] = src.cameras
-        pin_l[...] = src.landmarks
+        pin_c = torch.empty(state0.cameras.shape, dtype=torch.float64, pin_memory=True).numpy()
+        pin_l = torch.empty(state0.landmarks.shape, dtype=torch.float64, pin_memory=True).numpy()
+        pin_c[...] = state0.cameras
+        pin_l[...] = state0.landmarks
         st_in = pv.ProjectiveState(pin_c, pin_l)
         pv.lm_minimize(problem, st_in, 1, pv.SolverConfig(max_outer_iterations=1), dp=dp)  # warm
         barrier()
+        decisions = []
         t = time.perf_counter()
-        st_out, trace = pv.lm_minimize(problem, st_in, 1, cfgK, dp=dp)
+        st_out, trace = pv.lm_minimize(problem, st_in, 1, cfgK, dp=dp, decisions=decisions)
         dt = max_over_ranks(time.perf_counter() - t)
         n_it = len(trace.records) - 1
+        e_orders = [d["order"] for d in decisions]
         bytes_state = st_in.cameras.nbytes + st_in.landmarks.nbytes
         e2e = {"value": n_o * n_it / dt, "unit": "obs/s",
                "h2d_bytes_per_step": bytes_state / n_it,
-               "d2h_bytes_per_step": (bytes_state + 8 * n_it) / n_it,
+               "d2h_bytes_per_step": (bytes_state + 8 * (n_it + 1)) / n_it,
                "ms_per_step": 1e3 * dt / n_it, "steps": n_it,
-               "api": "paper_2405_05079_b200.lm_minimize(problem, state, 1, max_outer_iterations=K)",
-               "note": "one call: pinned host state upload, K LM iterations, state download"}
+               "mean_power_order": float(np.mean(e_orders)),
+               "same_iterations_as_value": e_orders == orders,
+               "setup_s": max_over_ranks(setup_s),
+               "value_incl_setup": n_o * n_it / (dt + max_over_ranks(setup_s)),
+               "api": "paper_2405_05079_b200.lm_minimize(problem, state, 1, "
+                      "max_outer_iterations=K)",
+               "note": "one call: pinned host state upload, initial cost, LM iterations 1..K "
+                       "from the random start, state download; setup_s = DeviceProblem "
+                       "creation (graph sort, work lists, upload), paid once per problem"}
 
-    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
+    # ---- CPU baseline (rank 0, N=1 only): the reference at 1 and all host threads -----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, sp = cpu_port_lm(CPU_SAMPLE_FRACTION, iters=2)
-        cpu = {"value": v, "unit": "obs/s", "cores": 1, "kind": "port",
-               "sample": f"{CPU_SAMPLE_FRACTION:.0%} of vlarge landmarks "
-                         f"({sp.num_observations} obs), 2 stage-1 LM iterations, "
-                         f"{dt:.2f} s/iter, NumPy oracle port single-threaded"}
+        nthr = len(os.sched_getaffinity(0))
+        runs = [cpu_lm(CPU_SAMPLE_FRACTION, 2, t, warm=1 if t == 1 else 0)[0]
+                for t in sorted({1, nthr})]
+        best = max(runs, key=lambda r: r["obs_per_s"])
+        cpu = {"value": best["obs_per_s"], "unit": "obs/s", "cores": best["threads"],
+               "kind": best["kind"],
+               "sample": f"{CPU_SAMPLE_FRACTION:.0%} of vlarge landmarks ({best['n_obs']} obs), "
+                         f"LM iterations 1..2 from the random start, "
+                         + ("stratba.lm_minimize (baseline/_ref)" if best["kind"] == "reference"
+                            else "NumPy oracle port"),
+               "by_threads": {str(r["threads"]): r["obs_per_s"] for r in runs},
+               "host": host_record()}
 
     if rank == 0:
         ws = (dp.info()["device_bytes"]) / 1e9
@@ -426,14 +546,18 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64",
                 "data": "synthetic (seeded BASELINE vlarge generator, SURVEY App. C)",
-                "config": {"workload": f"{args.config} stage-1 PoVar LM iteration",
+                "config": {"workload": f"{args.config} stage-1 PoVar LM iterations 1..K from "
+                                       "the random N(0,1) start",
                            "n_cameras": n_p, "n_landmarks": n_l, "n_obs": n_o,
                            "max_power_order": cfg.max_power_order, "power_threshold": 0.01,
                            "mean_power_order": float(np.mean(orders)) if orders else None,
+                           "power_orders": orders,
                            "l2": f"inputs larger than L2 (device working set {ws:.1f} GB)",
                            "parallelism": f"landmark-sharded dp{world}"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(), "spmv": spmv,
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "ms_per_term": spmv["ms_per_term"], "non_term_ms_per_step": non_term_ms,
+                "breakdown_ms_per_step": breakdown, "setup_s": setup_s, "spmv": spmv,
                 "stage2": stage2, "pcg": pcg}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -174,10 +174,11 @@ int pv_get_step(pv_ctx* ctx, double* dx, double* dl);
  * of length n_p*d (d = 12 stage 1, 11 stage 2) for the current linearization. */
 int pv_schur_apply(pv_ctx* ctx, int stage, const double* v, double* out);
 
-/* Timed power-series terms (no stop test), for the bench: runs n_terms terms on
- * the context stream and returns mean device ms per term of k_lm_reduce and of
- * k_cam (measured on block 0, scaled by the block count), the block count, and
- * the whole term (event to event) in ms[0..3]. */
+/* Timed power-series terms (no stop test), for the bench: runs n_terms terms on the
+ * context stream twice each -- once with CUDA events around every launch group, once
+ * back to back -- and returns per term: ms[0] the landmark reduces (all blocks), ms[1]
+ * the camera passes (all blocks, incl. the epilogue), ms[2] the block count, ms[3] the
+ * whole term (event to event, no events inside). */
 int pv_bench_terms(pv_ctx* ctx, int stage, int n_terms, float* ms);
 
 int pv_debug_get(pv_ctx* ctx, int which, double* out);

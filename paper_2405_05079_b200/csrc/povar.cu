@@ -56,6 +56,7 @@ struct pv_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> bev;  // per-launch timing events of pv_bench_terms
   std::string err;
   long long launches = 0;
   size_t device_bytes = 0;
@@ -1168,6 +1169,8 @@ void pv_destroy(pv_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto e : c->tev)
     if (e) cudaEventDestroy(e);
+  for (auto e : c->bev)
+    if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1492,38 +1495,51 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
   // seed s of block 0 from the current camera vector
   launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 0));
-  float acc[4] = {0, 0, 0, 0};
-  for (int i = 1; i <= n; ++i) {
-    // whole term timed end to end; per-kernel split measured on the first block
-    CK(cudaEventRecord(c->tev[0], c->stream));
-    launch_lm_reduce<S, LR_TERM>(c, 0, 1, 0);
-    CK(cudaEventRecord(c->tev[1], c->stream));
-    const int B = c->n_blk;
-    if (B > 1)
-      launch_cam<S, true, EP_NONE, true>(c, cam_args(0, 1, 1, 1, 2, 1 << 20, -1.0, 0));
-    else
-      launch_cam_last<S, EP_TERM>(c, 0, 1, 1, 1 << 20, -1.0, 0);
-    CK(cudaEventRecord(c->tev[2], c->stream));
-    for (int b = 1; b < B; ++b) {
+  const int B = c->n_blk;
+  // events around EVERY launch group of a term: per block the landmark reduce and the
+  // camera pass (the last block's camera group = its W t pass, the epilogue and block 0's
+  // next W^T v pass)
+  if (c->bev.size() < (size_t)(2 * B + 1)) {
+    for (auto e : c->bev) cudaEventDestroy(e);
+    c->bev.assign(2 * B + 1, nullptr);
+    for (auto& e : c->bev) CK(cudaEventCreate(&e));
+  }
+  double acc[4] = {0, 0, 0, 0};
+  auto term = [&](bool per_kernel) {
+    for (int b = 0; b < B; ++b) {
+      if (per_kernel) CK(cudaEventRecord(c->bev[2 * b], c->stream));
       launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 0);
+      if (per_kernel) CK(cudaEventRecord(c->bev[2 * b + 1], c->stream));
       if (b + 1 < B)
-        launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, 0, b + 1, b + 2, 1 << 20, -1.0,
-                                                       0));
+        launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, 1 << 20,
+                                                       -1.0, 0));
       else
-        launch_cam_last<S, EP_TERM>(c, b, b + 1, 0, 1 << 20, -1.0, 0);
+        launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, 1 << 20, -1.0, 0);
     }
+    if (per_kernel) CK(cudaEventRecord(c->bev[2 * B], c->stream));
+  };
+  for (int i = 0; i < n; ++i) {
+    // pass 1: the per-kernel split (the events add small gaps between launches)
+    term(true);
+    CK(cudaEventSynchronize(c->bev[2 * B]));
+    for (int b = 0; b < B; ++b) {
+      float a, d;
+      CK(cudaEventElapsedTime(&a, c->bev[2 * b], c->bev[2 * b + 1]));
+      CK(cudaEventElapsedTime(&d, c->bev[2 * b + 1], c->bev[2 * b + 2]));
+      acc[0] += a;
+      acc[1] += d;
+    }
+    acc[2] += B;
+    // pass 2: the whole term, back to back with no events inside
+    CK(cudaEventRecord(c->tev[0], c->stream));
+    term(false);
     CK(cudaEventRecord(c->tev[3], c->stream));
     CK(cudaEventSynchronize(c->tev[3]));
-    float a, b2, d;
-    CK(cudaEventElapsedTime(&a, c->tev[0], c->tev[1]));
-    CK(cudaEventElapsedTime(&b2, c->tev[1], c->tev[2]));
+    float d;
     CK(cudaEventElapsedTime(&d, c->tev[0], c->tev[3]));
-    acc[0] += a * B;   // extrapolated over blocks (blocks have equal observation counts)
-    acc[1] += b2 * B;
-    acc[2] += (float)B;
     acc[3] += d;
   }
-  for (int q = 0; q < 4; ++q) ms[q] = acc[q] / std::max(n, 1);
+  for (int q = 0; q < 4; ++q) ms[q] = (float)(acc[q] / std::max(n, 1));
 }
 
 

@@ -188,8 +188,9 @@ class DeviceProblem:
     def bench_terms(self, stage: int, n_terms: int) -> dict:
         ms = (ctypes.c_float * 4)()
         self._call("pv_bench_terms", int(stage), int(n_terms), ms)
-        # [0] k_lm_reduce, [1] k_cam (fused; part A when sharded), [2] allreduce + part B
-        return {"phase1_ms": ms[0], "phase2_ms": ms[1], "epilogue_ms": ms[2], "term_ms": ms[3]}
+        # per term: landmark reduces and camera passes summed over every block launch
+        # (events around each launch group), the block count, the whole term (no events)
+        return {"lm_reduce_ms": ms[0], "cam_ms": ms[1], "blocks": int(ms[2]), "term_ms": ms[3]}
 
     def debug(self, which: int) -> np.ndarray:
         sizes = {_lib.PV_DBG_U: (self.n_p, 144), _lib.PV_DBG_ULIN: (self.n_p, 144),

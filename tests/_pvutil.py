@@ -43,3 +43,16 @@ def reference_stratba():
     for sub in ("solvers", "pipeline", "bal_io", "evaluation", "riemannian", "objective"):
         importlib.import_module("stratba." + sub)
     return mod
+
+
+# achieved parity errors of the GPU tests: every check() is recorded and, when
+# PV_PARITY_REPORT names a file, written there at the end of the session (conftest.py)
+REPORT = []
+
+
+def check(label, err, tol):
+    """Assert ``err <= tol`` and record the achieved error next to its tolerance."""
+    import os
+    test = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    REPORT.append({"test": test, "quantity": label, "error": float(err), "tol": float(tol)})
+    assert err <= tol, f"{label}: {err:.3e} > {tol:.0e}"

@@ -27,3 +27,13 @@ from _pvutil import golden  # noqa: E402
 @pytest.fixture(params=[0, 1, 2], ids=lambda s: f"mini{s}")
 def mini(request):
     return golden(f"mini_{request.param}.npz")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    import json
+
+    import _pvutil
+    path = os.environ.get("PV_PARITY_REPORT")
+    if path and _pvutil.REPORT:
+        Path(path).parent.mkdir(parents=True, exist_ok=True)
+        Path(path).write_text(json.dumps(_pvutil.REPORT, indent=1))

@@ -14,7 +14,7 @@ mini_s1.npz / mini_s2.npz  -- small random graphs (reference conftest style):
     solve_landmarks, total_cost; stage 2 uses project_blocks + BOTH damping.
 tiny_lm.npz  -- BASELINE tiny config: reference stage-1 lm_minimize (20 its),
     first-iteration power solve, stage-2 lm_minimize from the lifted result
-    (12 its) and its first riemannian_step.
+    (20 its) and its first riemannian_step.
 small_lm.npz -- BASELINE small config: reference stage-1 cost trace (50 its).
 pcg.npz      -- the PCG inner solver (solvers.py:153-187) on the mini graphs:
     schur_diag_blocks and pcg_schur_solve at three (tolerance, cap) settings for
@@ -32,7 +32,8 @@ pipeline_*   -- run_problem summaries / trace CSVs on tiny.bal.gz
 spectral.npz -- spectral_check (solvers.py:263-295) on the mini systems, with the dense top
     eigenvalue of U^-1 W V^+ W^T beside it.
 
-``python tests/golden/make_golden.py pcg|bal|spectral`` regenerates one group only.
+``python tests/golden/make_golden.py pcg|bal|spectral|traces`` regenerates one group only.
+Scale and edge-case fixtures: tests/golden/make_golden_scale.py.
 """
 
 from __future__ import annotations
@@ -191,12 +192,16 @@ def make_config_traces():
     out["s1_cams"], out["s1_lms"] = s1.cameras, s1.landmarks
     lifted = riemannian.lift_stage1_to_stage2(s1)
     out["s2_cams0"], out["s2_lms0"] = lifted.cameras, lifted.landmarks
-    cfg2 = solvers.SolverConfig(max_outer_iterations=12)
+    cfg2 = solvers.SolverConfig(max_outer_iterations=20)
     rep2 = riemannian.riemannian_step(ref_problem, lifted, cfg2, cfg2.initial_lambda)
     out["s2_it1_dx"], out["s2_it1_dl"] = rep2.pose_update, rep2.landmark_update
     out["s2_it1_order"] = rep2.power_order_used
     s2, tr2 = solvers.lm_minimize(ref_problem, lifted, 2, cfg2)
     out["s2_costs"] = np.array([r.cost for r in tr2.records])
+    # the default tolerance stops stage 2 after a few iterations; all 20 (north_star)
+    cfg20 = solvers.SolverConfig(max_outer_iterations=20, function_tolerance=1e-300)
+    _, tr20 = solvers.lm_minimize(ref_problem, lifted, 2, cfg20)
+    out["s2_costs20"] = np.array([r.cost for r in tr20.records])
     np.savez_compressed(OUT / "tiny_lm.npz", **out)
 
     problem, _ = synth.make_problem("small", 0)
@@ -418,6 +423,8 @@ if __name__ == "__main__":
         make_spectral()
     elif sys.argv[1:] == ["bal"]:
         make_bal()
+    elif sys.argv[1:] == ["traces"]:
+        make_config_traces()
     else:
         make_mini()
         make_config_traces()

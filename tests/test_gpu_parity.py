@@ -13,7 +13,7 @@ import math
 import numpy as np
 import pytest
 
-from _pvutil import golden, problem_from, rel
+from _pvutil import check, golden, problem_from, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -54,37 +54,38 @@ def test_stage1_blocks_and_power(pv, mini, tag, both):
                               dp=dp)
     n_p = dp.n_p
     U = dp.debug(_lib.PV_DBG_U).reshape(n_p, 12, 12)
-    assert rel(U, z[tag + "U"]) <= TOL
-    assert rel(dp.debug(_lib.PV_DBG_BP), z[tag + "b_p"]) <= TOL
+    check(tag + "U", rel(U, z[tag + "U"]), TOL)
+    check(tag + "b_p", rel(dp.debug(_lib.PV_DBG_BP), z[tag + "b_p"]), TOL)
     V6 = dp.debug(_lib.PV_DBG_V)
     Vref = z[tag + "V"]
     if both:  # golden V is damped in BOTH mode; compare the undamped off-diagonals
         iu = [(0, 1), (0, 2), (1, 2)]
-        assert rel(V6[:, [1, 2, 4]], np.stack([Vref[:, i, j] for i, j in iu], 1)) <= TOL
+        check(tag + "V(offdiag)", rel(V6[:, [1, 2, 4]], np.stack([Vref[:, i, j] for i, j in iu], 1)),
+              TOL)
     else:
         full = np.stack([V6[:, 0], V6[:, 1], V6[:, 2], V6[:, 3], V6[:, 4], V6[:, 5]], 1)
         ref = np.stack([Vref[:, 0, 0], Vref[:, 0, 1], Vref[:, 0, 2], Vref[:, 1, 1],
                         Vref[:, 1, 2], Vref[:, 2, 2]], 1)
-        assert rel(full, ref) <= TOL
+        check(tag + "V", rel(full, ref), TOL)
     Vp = dp.debug(_lib.PV_DBG_VPINV)
     Vpr = z[tag + "Vp"]
     ref = np.stack([Vpr[:, 0, 0], Vpr[:, 0, 1], Vpr[:, 0, 2], Vpr[:, 1, 1], Vpr[:, 1, 2],
                     Vpr[:, 2, 2]], 1)
-    assert rel(Vp, ref) <= 1e-9  # eigh vs Jacobi on cond(V) up to ~1e6
-    assert rel(dp.debug(_lib.PV_DBG_BL), z[tag + "b_l"]) <= TOL
+    check(tag + "V+", rel(Vp, ref), TOL)
+    check(tag + "b_l", rel(dp.debug(_lib.PV_DBG_BL), z[tag + "b_l"]), TOL)
     W = dp.debug(_lib.PV_DBG_W).reshape(-1, 12, 3)
-    assert rel(W, z[tag + "W"]) <= TOL
+    check(tag + "W", rel(W, z[tag + "W"]), TOL)
     # S'.v on a probe vector
-    assert rel(dp.schur_apply(1, z["probe12"]), z[tag + "coupling"]) <= TOL
+    check(tag + "S'v", rel(dp.schur_apply(1, z["probe12"]), z[tag + "coupling"]), TOL)
     # power series, both thresholds
     for t2, thr in (("thr", 0.01), ("zero", 0.0)):
         cfg = pv.SolverConfig(max_power_order=20, power_threshold=thr)
         rep = pv.power_schur_solve(sysm, cfg)
         assert rep.power_order_used == int(z[tag + f"pow_{t2}_order"])
         assert abs(rep.truncation_estimate - float(z[tag + f"pow_{t2}_trunc"])) <= 1e-9
-        assert rel(rep.pose_update, z[tag + f"pow_{t2}_dx"]) <= TOL
-        assert rel(rep.landmark_update, z[tag + f"pow_{t2}_dl"]) <= TOL
-    assert rel(dp.debug(_lib.PV_DBG_RHS)[:, :12].ravel(), z[tag + "rhs"]) <= TOL
+        check(tag + f"dx({t2})", rel(rep.pose_update, z[tag + f"pow_{t2}_dx"]), TOL)
+        check(tag + f"dl({t2})", rel(rep.landmark_update, z[tag + f"pow_{t2}_dl"]), TOL)
+    check(tag + "rhs", rel(dp.debug(_lib.PV_DBG_RHS)[:, :12].ravel(), z[tag + "rhs"]), TOL)
 
 
 def test_stage2_blocks_and_power(pv, mini):
@@ -95,24 +96,25 @@ def test_stage2_blocks_and_power(pv, mini):
     sysm = pv.assemble_system(dp.problem, st, 2, float(z["s2_lam"]), "both", dp=dp)
     n_p = dp.n_p
     U = dp.debug(_lib.PV_DBG_U).reshape(n_p, 12, 12)[:, :11, :11]
-    assert rel(U, z["s2_U"]) <= TOL
-    assert rel(dp.debug(_lib.PV_DBG_BP)[:, :11], z["s2_b_p"]) <= TOL
-    assert rel(dp.debug(_lib.PV_DBG_BL), z["s2_b_l"]) <= TOL
+    check("s2_U", rel(U, z["s2_U"]), TOL)
+    check("s2_b_p", rel(dp.debug(_lib.PV_DBG_BP)[:, :11], z["s2_b_p"]), TOL)
+    check("s2_b_l", rel(dp.debug(_lib.PV_DBG_BL), z["s2_b_l"]), TOL)
     W = dp.debug(_lib.PV_DBG_W).reshape(-1, 12, 3)[:, :11, :]
-    assert rel(W, z["s2_W"]) <= TOL
-    assert rel(dp.schur_apply(2, z["probe11"]), z["s2_coupling"]) <= 1e-9
+    check("s2_W", rel(W, z["s2_W"]), TOL)
+    check("s2_S'v", rel(dp.schur_apply(2, z["probe11"]), z["s2_coupling"]), TOL)
     rhs = dp.debug(_lib.PV_DBG_RHS)
     cfg = pv.SolverConfig(max_power_order=20, power_threshold=0.01)
     rep = pv.power_schur_solve(sysm, cfg)
     rhs = dp.debug(_lib.PV_DBG_RHS)[:, :11].ravel()
-    assert np.linalg.norm(rhs - z["s2_rhs"]) <= 1e-9 * np.linalg.norm(z["s2_b_p"])
+    check("s2_rhs/|b_p|", np.linalg.norm(rhs - z["s2_rhs"]) / np.linalg.norm(z["s2_b_p"]), 1e-9)
+    check("s2_rhs", rel(rhs, z["s2_rhs"]), 1e-6)
     assert rep.power_order_used == int(z["s2_pow_thr_order"])
-    assert rel(rep.pose_update, z["s2_pow_thr_dx"]) <= 1e-8
+    check("s2_dx", rel(rep.pose_update, z["s2_pow_thr_dx"]), 1e-8)
     # trial state through the device retraction
     assert dp.trial(2)
     trial = dp.get_state(trial=True)
-    assert rel(trial.cameras, z["s2_trial_cams"]) <= 1e-8
-    assert rel(dp.cost(2, trial=True), z["s2_trial_cost"]) <= 1e-8
+    check("s2_trial_cams", rel(trial.cameras, z["s2_trial_cams"]), 1e-8)
+    check("s2_trial_cost", rel(dp.cost(2, trial=True), z["s2_trial_cost"]), 1e-8)
 
 
 @pytest.mark.parametrize("tag,stage,kw", [
@@ -158,10 +160,10 @@ def test_tiny_stage2_trace(pv):
     z = golden("tiny_lm.npz")
     dp = _dp(pv, z)
     st = _state(pv, z, "s2_cams0", "s2_lms0")
-    rep = pv.riemannian_step(dp.problem, st, pv.SolverConfig(max_outer_iterations=12), dp=dp)
+    rep = pv.riemannian_step(dp.problem, st, pv.SolverConfig(max_outer_iterations=20), dp=dp)
     assert rep.power_order_used == int(z["s2_it1_order"])
     assert rel(rep.pose_update, z["s2_it1_dx"]) <= 1e-8
-    final, trace = pv.lm_minimize(dp.problem, st, 2, pv.SolverConfig(max_outer_iterations=12),
+    final, trace = pv.lm_minimize(dp.problem, st, 2, pv.SolverConfig(max_outer_iterations=20),
                                   dp=dp)
     costs = np.array([r.cost for r in trace.records])
     ref = z["s2_costs"]
@@ -169,6 +171,21 @@ def test_tiny_stage2_trace(pv):
     np.testing.assert_allclose(costs, ref, rtol=1e-6, atol=0)
     norms = np.linalg.norm(final.cameras.reshape(-1, 12), axis=1)
     assert np.abs(norms - 1).max() <= 1e-12
+    # all 20 iterations (function tolerance off): past convergence the accepted decreases
+    # are at rounding level, so the accept decisions are compared where the reference's
+    # relative decrease exceeds 1e-10 and the costs everywhere
+    _, trace = pv.lm_minimize(dp.problem, st, 2,
+                              pv.SolverConfig(max_outer_iterations=20,
+                                              function_tolerance=1e-300), dp=dp)
+    costs = np.array([r.cost for r in trace.records])
+    ref = z["s2_costs20"]
+    assert len(costs) == len(ref) == 21
+    print(f"tiny stage-2, 20 iterations: max relative cost difference "
+          f"{np.max(np.abs(costs - ref) / ref):.2e}")
+    np.testing.assert_allclose(costs, ref, rtol=1e-6, atol=0)
+    clear = (ref[:-1] - ref[1:]) / ref[:-1] > 1e-10
+    ours = costs[1:] < costs[:-1]
+    assert np.array_equal(ours[clear], (ref[1:] < ref[:-1])[clear])
 
 
 def test_small_stage1_trace(pv):

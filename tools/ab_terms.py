@@ -44,6 +44,6 @@ for rnd in range(rounds):
         r = dp.bench_terms(stage, 10)
         res[i].append(r["term_ms"])
         print(f"round {rnd} variant {i} {var}: term {r['term_ms']:.4f} ms "
-              f"(lm_reduce~{r['phase1_ms']:.3f} cam~{r['phase2_ms']:.3f})", flush=True)
+              f"(lm_reduce~{r['lm_reduce_ms']:.3f} cam~{r['cam_ms']:.3f})", flush=True)
 for i, var in enumerate(variants):
     print(f"variant {i} {var}: best term {min(res[i]):.4f} ms  mean {np.mean(res[i]):.4f}")

@@ -22,5 +22,5 @@ for mb in mbs:
     r = dp.bench_terms(1, 10)
     info = dp.info()
     print(f"{os.environ.get('PV_LIB_PATH', 'default')} budget {mb} MB: B={info['blocks']} "
-          f"wpc={info['warps_per_cam']} lm_reduce~{r['phase1_ms']:.4f} cam~{r['phase2_ms']:.4f} "
+          f"wpc={info['warps_per_cam']} lm_reduce~{r['lm_reduce_ms']:.4f} cam~{r['cam_ms']:.4f} "
           f"term {r['term_ms']:.4f} ms", flush=True)

@@ -38,5 +38,5 @@ for mb, (ps, pt, pss), disc in itertools.product(blocks, pols, discs):
     dp.bench_terms(stage, 2)
     r = dp.bench_terms(stage, 10)
     print(f"block={mb:5d}MB B={dp.info()['blocks']:3d} pol={ps}{pt}{pss} disc={disc}  "
-          f"lm_reduce~{r['phase1_ms']:.3f} cam~{r['phase2_ms']:.3f} term={r['term_ms']:.3f} ms  "
+          f"lm_reduce~{r['lm_reduce_ms']:.3f} cam~{r['cam_ms']:.3f} term={r['term_ms']:.3f} ms  "
           f"{n_o / r['term_ms'] / 1e6:.2f} Gobs/s", flush=True)
