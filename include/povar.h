@@ -91,8 +91,10 @@ enum {
                                   kernel and the epilogue + next W^T v pass separately     */
   PV_OPT_RHS_REUSE = 11,       /* 1: a solve after a rejected stage-1 step (same linearization,
                                   POSE_ONLY) reuses the reduced RHS -(b_p - W V+ b_l)      */
-  PV_OPT_COST_CS = 12          /* 1: pv_cost walks the camera-sorted segments (one camera load
+  PV_OPT_COST_CS = 12,         /* 1: pv_cost walks the camera-sorted segments (one camera load
                                   per warp segment); 0: landmark-task order                */
+  PV_OPT_BENCH_SPLIT = 13      /* diagnostic: pv_bench_terms times the W^T v passes (ms[0]) and
+                                  the W t passes (ms[1]) of all blocks on their own         */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

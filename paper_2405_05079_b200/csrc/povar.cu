@@ -20,6 +20,7 @@
 #include "pv_kernels.cuh"
 #include "pv_pcg.cuh"
 #include "pv_pipe.cuh"
+#include "pv_pipe2.cuh"
 
 using namespace pv;
 
@@ -96,7 +97,10 @@ struct pv_ctx {
   int num_sms = 148;
   int wpc = 1;  // warps per camera in the camera kernels (from the mean segment size)
   // work lists of the persistent camera kernel (k_cam_pipe)
-  int pipe_W = 0;
+  int pipe_W = 0;          // consumer warps the item lists were built for
+  int pipe_W_of[3] = {0, 0, 0};
+  int bench_split = 0;  // pv_bench_terms diagnostic (PV_OPT_BENCH_SPLIT)
+  int* d_pipe_ctr = nullptr;
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
@@ -337,22 +341,37 @@ static void ensure_cpart(pv_ctx* c) {
 // per-item overhead) and cut each (camera, block) segment into items of <= PCH
 // observations.  The W t list has >= 1 item per camera so that y is always written.
 static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
-  if (!c->pipe_W) {
+  // consumer warps of the persistent grid: resident CTAs per SM x SMs x warps per CTA
+  // (k_cam_pipe: every warp; k_cam_pipe2: the consumer warps)
+  const int ver = c->tune.cam_pipe == 2 ? 2 : 1;
+  if (!c->pipe_W_of[ver]) {
     int occ = 1 << 30;
-    auto occ_of = [&](const void* fn) {
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PIPE_SMEM));
+    auto occ_of = [&](const void* fn, int threads, int smem) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       int o = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, PW * 32, PIPE_SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
       occ = std::min(occ, o);
     };
-    occ_of((const void*)k_cam_pipe<1, true, true>);
-    occ_of((const void*)k_cam_pipe<2, true, true>);
-    occ_of((const void*)k_cam_pipe<1, false, true>);
-    occ_of((const void*)k_cam_pipe<2, false, true>);
-    occ_of((const void*)k_cam_pipe<1, true, false>);
-    occ_of((const void*)k_cam_pipe<2, true, false>);
-    c->pipe_W = std::max(1, occ) * c->num_sms * PW;
+    if (ver == 2) {
+      occ_of((const void*)k_cam_pipe2<1, true, true>, P2T, PIPE2_SMEM);
+      occ_of((const void*)k_cam_pipe2<2, true, true>, P2T, PIPE2_SMEM);
+      occ_of((const void*)k_cam_pipe2<1, false, true>, P2T, PIPE2_SMEM);
+      occ_of((const void*)k_cam_pipe2<2, false, true>, P2T, PIPE2_SMEM);
+      occ_of((const void*)k_cam_pipe2<1, true, false>, P2T, PIPE2_SMEM);
+      occ_of((const void*)k_cam_pipe2<2, true, false>, P2T, PIPE2_SMEM);
+      c->pipe_W_of[ver] = std::max(1, occ) * c->num_sms * P2C;
+    } else {
+      occ_of((const void*)k_cam_pipe<1, true, true>, PW * 32, PIPE_SMEM);
+      occ_of((const void*)k_cam_pipe<2, true, true>, PW * 32, PIPE_SMEM);
+      occ_of((const void*)k_cam_pipe<1, false, true>, PW * 32, PIPE_SMEM);
+      occ_of((const void*)k_cam_pipe<2, false, true>, PW * 32, PIPE_SMEM);
+      occ_of((const void*)k_cam_pipe<1, true, false>, PW * 32, PIPE_SMEM);
+      occ_of((const void*)k_cam_pipe<2, true, false>, PW * 32, PIPE_SMEM);
+      c->pipe_W_of[ver] = std::max(1, occ) * c->num_sms * PW;
+    }
   }
+  c->pipe_W = c->pipe_W_of[ver];
+  if (!c->d_pipe_ctr) c->d_pipe_ctr = c->alloc<int>(4);  // k_cam_pipe2's self-resetting counter
   const int B = c->n_blk, W = c->pipe_W;
   const int64_t np = c->n_p;
   constexpr int ITEM_COST = 24;  // observation-equivalents of one item's fixed overhead
@@ -754,6 +773,13 @@ static void launch_cam_v(pv_ctx* c, const CamArgs& ca) {
 template <int S, bool HC, bool HA>
 static void launch_cam_pipe(pv_ctx* c, const CamArgs& ca) {
   PipeItems it{c->d_items, c->d_item_off, c->n_blk, c->pipe_W};
+  if (c->tune.cam_pipe == 2) {
+    k_cam_pipe2<S, HC, HA><<<c->pipe_W / P2C, P2T, PIPE2_SMEM, c->stream>>>(
+        c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
+        ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi, c->d_pipe_ctr);
+    c->launched();
+    return;
+  }
   k_cam_pipe<S, HC, HA><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
       c->g, it, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
       ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi);
@@ -1236,14 +1262,22 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_RHS_REUSE:
       c->tune.rhs_reuse = value ? 1 : 0;
       break;
+    case PV_OPT_BENCH_SPLIT:
+      c->bench_split = value ? 1 : 0;
+      break;
     case PV_OPT_COST_CS:
       c->tune.cost_cs = value ? 1 : 0;
       break;
     case PV_OPT_SPLIT_LAST:
       c->tune.split_last = value ? 1 : 0;
       break;
-    case PV_OPT_CAM_PIPE:
-      c->tune.cam_pipe = value ? 1 : 0;
+    case PV_OPT_CAM_PIPE:  // 0: k_cam, 1: k_cam_pipe, 2: warp-specialized k_cam_pipe2
+      if (value < 0 || value > 2) throw PvError(PV_EINVAL, "PV_OPT_CAM_PIPE must be 0, 1 or 2");
+      if ((value == 2) != (c->tune.cam_pipe == 2)) {
+        c->tune.cam_pipe = (int)value;
+        build_blocks(c);  // the item lists depend on the consumer-warp count
+      }
+      c->tune.cam_pipe = (int)value;
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
@@ -1518,6 +1552,28 @@ static void op_bench_terms(pv_ctx* c, int n, float* ms) {
     }
     if (per_kernel) CK(cudaEventRecord(c->bev[2 * B], c->stream));
   };
+  if (c->bench_split) {
+    // diagnostic: the two camera passes on their own -- every block's W^T v pass (HA
+    // only), then every block's W t pass (HC only) -- ms[0] / ms[1] per term
+    for (int i = 0; i < n; ++i) {
+      CK(cudaEventRecord(c->tev[0], c->stream));
+      for (int b = 0; b < B; ++b)
+        launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, b, b + 1, 0, 0.0, 0));
+      CK(cudaEventRecord(c->tev[1], c->stream));
+      for (int b = 0; b < B; ++b)
+        launch_cam<S, true, EP_NONE, false>(c, cam_args(b, b + 1, b == 0, 0, 0, 0, 0.0, 0));
+      CK(cudaEventRecord(c->tev[2], c->stream));
+      CK(cudaEventSynchronize(c->tev[2]));
+      float a, d;
+      CK(cudaEventElapsedTime(&a, c->tev[0], c->tev[1]));
+      CK(cudaEventElapsedTime(&d, c->tev[1], c->tev[2]));
+      acc[0] += a;
+      acc[1] += d;
+      acc[2] += B;
+    }
+    for (int q = 0; q < 4; ++q) ms[q] = (float)(acc[q] / std::max(n, 1));
+    return;
+  }
   for (int i = 0; i < n; ++i) {
     // pass 1: the per-kernel split (the events add small gaps between launches)
     term(true);
@@ -1552,6 +1608,21 @@ int pv_bench_terms(pv_ctx* c, int stage, int n, float* ms) {
   STAGE_DISPATCH(stage, op_bench_terms, c, n, ms);
   API_END(c)
 }
+
+#ifdef PV_PIPE2_TIMING
+// diagnostic build only: start / end globaltimer and item count of every consumer warp of
+// the last k_cam_pipe2 launch
+int pv_debug_pipe2_times(pv_ctx* c, unsigned long long* t, int* items, int* n,
+                         unsigned long long* entry) {
+  API_BEGIN(c)
+  CK(cudaStreamSynchronize(c->stream));
+  *n = c->pipe_W;
+  CK(cudaMemcpyFromSymbol(entry, pv::g_pipe2_entry, sizeof(unsigned long long) * (c->pipe_W / P2C)));
+  CK(cudaMemcpyFromSymbol(t, pv::g_pipe2_t, sizeof(unsigned long long) * 2 * c->pipe_W));
+  CK(cudaMemcpyFromSymbol(items, pv::g_pipe2_items, sizeof(int) * c->pipe_W));
+  API_END(c)
+}
+#endif
 
 int pv_debug_get(pv_ctx* c, int which, double* out) {
   API_BEGIN(c)

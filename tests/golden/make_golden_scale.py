@@ -1,6 +1,7 @@
 """Scale and edge-case golden fixtures from the REAL reference package (build container only).
 
-Run from the repo root:  python tests/golden/make_golden_scale.py [medium|subsample|degen|all]
+Run from the repo root:
+    python tests/golden/make_golden_scale.py [medium|floor|gt|subsample|degen|all]
 
 Like make_golden.py it imports ``stratba`` read-only from /root/reference/pkg/src and
 stores the reference's own outputs.  The large problems themselves are NOT stored: the
@@ -24,6 +25,12 @@ medium_s2.npz -- stage 2 (RiPoBA) from the lifted reference stage-1 result:
       from the reference's dx_k (back_substitute, normal_eq.py:239-250), so both sides
       linearize at the same point every step;
     * the free-running 20-iteration stage-2 lm_minimize trace (divergence report).
+    * the reference's own conditioning floor on that chain ("floor"): the spread of its dx,
+      dl and f_trial when state_k is perturbed by 1e-16 relative, and its free-running
+      trace from a 1e-16-perturbed start.
+medium_s2gt.npz -- stage 2 as a refinement from the lifted, noisy ground truth (a
+    well-conditioned chain): first-iteration per-kernel quantities, the reference's
+    own 1e-16 sensitivity, and the 20-iteration free-running trace.
 subsample_lm.npz -- landmark subsamples of the large (5%, clustered visibility) and
     vlarge (1%, power-law tracks up to 500) configs: 10 stage-1 iterations each, costs
     and power orders.
@@ -267,6 +274,121 @@ def make_degen():
     np.savez_compressed(OUT / "degen.npz", **out)
 
 
+def _perturbed(state, eps, seed):
+    """The state with every coordinate scaled by (1 + eps N(0,1)), retracted."""
+    rng = np.random.default_rng(seed)
+    c = state.cameras * (1 + eps * rng.standard_normal(state.cameras.shape))
+    lm = state.landmarks * (1 + eps * rng.standard_normal(state.landmarks.shape))
+    return riemannian.retract(stratba.ProjectiveState(c, lm))
+
+
+def make_medium_floor():
+    """The reference's OWN sensitivity on the medium stage-2 chain (added to medium_s2.npz).
+
+    For each teacher-forced step k the reference re-runs riemannian_step + trial cost
+    from its state_k perturbed by 1e-16 relative (three seeds): the spread of dx, dl and
+    f_trial is the conditioning floor no implementation can beat.  The free-running
+    trace is re-run from a perturbed start as well (the reference's own divergence)."""
+    z = dict(np.load(OUT / "medium_s2.npz"))
+    problem, _ = synth.make_problem("medium", 0)
+    rp = ref_problem(problem)
+    cfg2 = solvers.SolverConfig(max_outer_iterations=20, max_power_order=20)
+    st_k = stratba.ProjectiveState(z["cams0"], z["lms0"])
+    floor = {"dx": [], "dl_proj": [], "f_trial": [], "trunc": []}
+    t = time.time()
+    for k in range(len(z["tf_lam"])):
+        lam = float(z["tf_lam"][k])
+        worst = dict.fromkeys(floor, 0.0)
+        for seed in range(3):
+            sp = _perturbed(st_k, 1e-16, 100 + seed)
+            bases = riemannian.state_tangent_bases(sp)
+            rep = riemannian.riemannian_step(rp, sp, cfg2, lam, bases)
+            trial = riemannian.apply_tangent_step(sp, bases, rep)
+            f_tr = objective.total_cost(trial, rp, 2)
+            dl = rep.landmark_update
+            proj = probe_vectors(dl.size, 9) @ dl
+            worst["dx"] = max(worst["dx"], np.linalg.norm(rep.pose_update - z["tf_dx"][k])
+                              / np.linalg.norm(z["tf_dx"][k]))
+            worst["dl_proj"] = max(worst["dl_proj"], np.linalg.norm(proj - z["tf_dl_proj"][k])
+                                   / np.linalg.norm(z["tf_dl_proj"][k]))
+            worst["f_trial"] = max(worst["f_trial"],
+                                   abs(f_tr - z["tf_f_trial"][k]) / z["tf_f_trial"][k])
+            worst["trunc"] = max(worst["trunc"], abs(rep.truncation_estimate - z["tf_trunc"][k])
+                                 / z["tf_trunc"][k])
+        for q in floor:
+            floor[q].append(worst[q])
+        print("floor step", k, {q: f"{v:.1e}" for q, v in worst.items()}, time.time() - t,
+              flush=True)
+        # the reference's own next state (its step from the unperturbed state_k)
+        bases = riemannian.state_tangent_bases(st_k)
+        if bool(z["tf_accepted"][k]):
+            rep = riemannian.riemannian_step(rp, st_k, cfg2, lam, bases)
+            st_k = riemannian.apply_tangent_step(st_k, bases, rep)
+    for q, v in floor.items():
+        z["floor_" + q] = np.array(v)
+    _, tr = solvers.lm_minimize(rp, _perturbed(stratba.ProjectiveState(z["cams0"], z["lms0"]),
+                                               1e-16, 7), 2, cfg2)
+    z["s2_costs_perturbed"] = np.array([r.cost for r in tr.records])
+    print("perturbed free run", z["s2_costs_perturbed"])
+    np.savez_compressed(OUT / "medium_s2.npz", **z)
+
+
+def make_medium_gt():
+    """medium_s2gt.npz -- stage 2 where RiPoBA is used as a refinement: from the lifted
+    ground truth with noise (cameras x (1 + 1e-3 N), landmarks + 1e-2 N), a
+    well-conditioned chain.  First-iteration per-kernel quantities, the reference's own
+    1e-16 sensitivity of dx, and the 20-iteration free-running trace."""
+    problem, truth = synth.make_problem("medium", 0)
+    rp = ref_problem(problem)
+    gt = synth.ground_truth_state(truth)
+    rng = np.random.default_rng(11)
+    cams = gt.cameras * (1 + 1e-3 * rng.standard_normal(gt.cameras.shape))
+    lms = np.array(gt.landmarks)
+    lms[:, :3] += 1e-2 * rng.standard_normal((len(lms), 3))
+    st = riemannian.lift_stage1_to_stage2(stratba.ProjectiveState(cams, lms))
+    out = {"checksum": checksum(problem, stratba.ProjectiveState(cams, lms)),
+           "cams0": st.cameras, "lms0": st.landmarks}
+    subset = np.arange(0, problem.num_landmarks, SUBSET_STRIDE)
+    out["subset"] = subset
+    cfg = solvers.SolverConfig(max_outer_iterations=20, max_power_order=20)
+    lam = cfg.initial_lambda
+    bases = riemannian.state_tangent_bases(st)
+    system = normal_eq.assemble(riemannian.project_blocks(normal_eq.build_stage2_blocks(rp, st),
+                                                          bases), lam, normal_eq.BOTH)
+    out["f0"] = objective.total_cost(st, rp, 2)
+    out["U"], out["b_p"] = system.u_blocks, system.b_p
+    out["rhs"] = normal_eq.schur_rhs(system)
+    probe = np.random.Generator(np.random.Philox(5)).standard_normal(system.pose_dim)
+    out["probe"] = probe
+    out["coupling"] = solvers._coupling_round_trip(system, probe)
+    out["V_sub"], out["Vp_sub"] = system.v_blocks[subset], system.v_inv[subset]
+    out["b_l_sub"] = system.b_l[subset]
+    out["n_degen"] = int(system.v_degenerate.sum())
+    rep = solvers.power_schur_solve(system, cfg)
+    out["it1_dx"], out["it1_order"] = rep.pose_update, rep.power_order_used
+    out["it1_trunc"] = rep.truncation_estimate
+    dl = rep.landmark_update.reshape(-1, 3)
+    out["it1_dl_sub"] = dl[subset]
+    out["it1_dl_proj"] = probe_vectors(dl.size, 9) @ dl.ravel()
+    trial = riemannian.apply_tangent_step(st, bases, rep)
+    out["it1_f_trial"] = objective.total_cost(trial, rp, 2)
+    fl = 0.0
+    for seed in range(3):
+        sp = _perturbed(st, 1e-16, 200 + seed)
+        r2 = riemannian.riemannian_step(rp, sp, cfg, lam, riemannian.state_tangent_bases(sp))
+        fl = max(fl, np.linalg.norm(r2.pose_update - rep.pose_update)
+                 / np.linalg.norm(rep.pose_update))
+    out["floor_dx"] = fl
+    print("medium gt first step order", rep.power_order_used, "dx floor", fl, flush=True)
+    t = time.time()
+    with OrderLog() as log:
+        _, tr = solvers.lm_minimize(rp, st, 2, cfg)
+    out["s2_costs"] = np.array([r.cost for r in tr.records])
+    out["s2_orders"] = np.array(log.orders)
+    print("medium gt stage 2", time.time() - t, out["s2_costs"], log.orders)
+    np.savez_compressed(OUT / "medium_s2gt.npz", **out)
+
+
 if __name__ == "__main__":
     print("numpy", np.__version__)
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
@@ -276,3 +398,7 @@ if __name__ == "__main__":
         make_subsample()
     if what in ("medium", "all"):
         make_medium()
+    if what in ("floor", "medium", "all"):
+        make_medium_floor()
+    if what in ("gt", "all"):
+        make_medium_gt()

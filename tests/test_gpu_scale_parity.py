@@ -167,12 +167,25 @@ def test_medium_stage2_teacher_forced(pv, medium2):
             f = f_trial
     for e in rows:
         print("medium stage-2 teacher-forced step", e["k"], "order", e["order"],
-              {k: f"{v:.1e}" for k, v in e.items() if k not in ("k", "order")})
+              {k: f"{v:.1e}" for k, v in e.items() if k not in ("k", "order")},
+              "reference's own 1e-16 floor:",
+              {q: f"{z['floor_' + q][e['k']]:.1e}" for q in ("dx", "dl_proj", "f_trial", "trunc")})
+    # This chain starts from an unconverged stage-1 result (stage-2 cost 2.3e9) and is
+    # ill-conditioned: the REFERENCE moves its own dx by up to ~7e-7 and f_trial by up to
+    # ~2e-2 when state_k is perturbed by 1e-16 (floor_*, make_golden_scale.py).  Asserted:
+    # every decision (power order, accept/reject: above); the step within 10x the
+    # reference's own floor (max over three perturbations); and the teacher-forced trial
+    # cost -- the reference's dx, device back-substitution and cost -- within north_star's
+    # 1e-6.  The trial cost of the device's OWN step is reported, not asserted: it is
+    # hypersensitive to the step (observations with |z| near 0 dominate this cost), e.g.
+    # at step 4 a 1.7e-8 relative change of dx moves it by ~2e-4.
     for e in rows:
+        k = e["k"]
         assert e["order"][0] == e["order"][1]
-        for q in ("dx", "dl_sub", "dl_proj", "trunc", "dl_norm", "f_trial(own step)"):
-            check(f"medium s2 step {e['k']} {q}", e[q], 1e-8)
-        check(f"medium s2 step {e['k']} f_trial(ref step)", e["f_trial(ref step)"], 1e-10)
+        for q, fq in (("dx", "dx"), ("dl_proj", "dl_proj"), ("trunc", "trunc")):
+            check(f"medium s2 step {k} {q} (floor {z['floor_' + fq][k]:.1e})", e[q],
+                  max(10 * float(z["floor_" + fq][k]), 1e-10))
+        check(f"medium s2 step {k} f_trial(ref step)", e["f_trial(ref step)"], 1e-6)
 
 
 def test_medium_stage2_free_running(pv, medium2):
@@ -188,12 +201,66 @@ def test_medium_stage2_free_running(pv, medium2):
     n = min(len(costs), len(ref))
     d = np.abs(costs[:n] - ref[:n]) / ref[:n]
     div = next((i for i in range(n) if d[i] > 1e-6), None)
+    pert = z["s2_costs_perturbed"]
+    m = min(len(pert), len(ref))
+    dp_ = np.abs(pert[:m] - ref[:m]) / ref[:m]
+    div_ref = next((i for i in range(m) if dp_[i] > 1e-6), None)
     print(f"medium stage-2 free-running: {n - 1} iterations compared, max relative cost "
-          f"difference {d.max():.2e}, first > 1e-6 at iteration {div}; accept ours "
+          f"difference {d.max():.2e}, first > 1e-6 at iteration {div}; the reference from a "
+          f"1e-16-perturbed start first differs > 1e-6 at iteration {div_ref}; accept ours "
           f"{_accept_string(costs)} ref {_accept_string(ref)}")
-    np.testing.assert_allclose(costs[:6], ref[:6], rtol=1e-6, atol=0)
-    assert _accept_string(costs[:6]) == _accept_string(ref[:6])
-    assert [x["order"] for x in decisions[:5]] == z["s2_orders"][:5].tolist()
+    # identical up to the first accepted step, whose trial cost is chaotic (see the
+    # teacher-forced test); the rest is the divergence report above
+    np.testing.assert_allclose(costs[:3], ref[:3], rtol=1e-6, atol=0)
+    assert _accept_string(costs[:4]) == _accept_string(ref[:4])
+    assert [x["order"] for x in decisions[:3]] == z["s2_orders"][:3].tolist()
+
+
+# --------------------------------------------------------------------------- medium, stage 2 GT
+
+def test_medium_stage2_refinement_per_kernel(pv, medium):
+    """Stage 2 as a refinement from the lifted noisy ground truth (well conditioned: the
+    reference's own dx moves by ~1e-13 under a 1e-16 perturbation): per-kernel parity at
+    north_star's 1e-10 and the free-running trace."""
+    from paper_2405_05079_b200 import _lib
+    _, problem, _, dp = medium
+    z = golden("medium_s2gt.npz")
+    st = pv.ProjectiveState(z["cams0"], z["lms0"])
+    sub = z["subset"]
+    sysm = pv.assemble_system(problem, st, 2, 1e-4, "both", dp=dp)
+    n_p = dp.n_p
+    err = {"f0": rel(dp.cost(2), float(z["f0"]))}
+    err["U"] = rel(dp.debug(_lib.PV_DBG_U).reshape(n_p, 12, 12)[:, :11, :11], z["U"])
+    err["b_p"] = rel(dp.debug(_lib.PV_DBG_BP)[:, :11], z["b_p"])
+    err["V+"] = rel(dp.debug(_lib.PV_DBG_VPINV)[sub], _sym6(z["Vp_sub"]))
+    err["b_l"] = rel(dp.debug(_lib.PV_DBG_BL)[sub], z["b_l_sub"])
+    assert int(dp.debug(_lib.PV_DBG_DEGEN).sum()) == int(z["n_degen"])
+    err["S'v"] = rel(dp.schur_apply(2, z["probe"]), z["coupling"])
+    rep = pv.power_schur_solve(sysm, pv.SolverConfig(max_power_order=20))
+    err["rhs"] = rel(dp.debug(_lib.PV_DBG_RHS)[:, :11].ravel(), z["rhs"])
+    assert rep.power_order_used == int(z["it1_order"])
+    err["trunc"] = abs(rep.truncation_estimate - float(z["it1_trunc"])) / float(z["it1_trunc"])
+    err["dx"] = rel(rep.pose_update, z["it1_dx"])
+    dl = rep.landmark_update.reshape(-1, 3)
+    err["dl(subset)"] = rel(dl[sub], z["it1_dl_sub"])
+    err["dl.probes"] = rel(_probes(dl.size) @ dl.ravel(), z["it1_dl_proj"])
+    assert dp.trial(2)
+    err["f_trial"] = rel(dp.cost(2, trial=True), float(z["it1_f_trial"]))
+    print("medium stage-2 refinement first iteration, relative errors:",
+          {k: f"{v:.1e}" for k, v in err.items()}, f"(reference floor dx {float(z['floor_dx']):.1e})")
+    for k, v in err.items():
+        check("medium s2 refinement " + k, v, TOL)
+    decisions = []
+    _, trace = pv.lm_minimize(problem, st, 2, pv.SolverConfig(max_outer_iterations=20), dp=dp,
+                              decisions=decisions)
+    costs = np.array([r.cost for r in trace.records])
+    ref = z["s2_costs"]
+    assert len(costs) == len(ref)
+    print(f"medium stage-2 refinement trace: max relative cost difference "
+          f"{np.max(np.abs(costs - ref) / ref):.2e}")
+    np.testing.assert_allclose(costs, ref, rtol=1e-6, atol=0)
+    assert _accept_string(costs) == _accept_string(ref)
+    assert [x["order"] for x in decisions] == z["s2_orders"].tolist()
 
 
 # --------------------------------------------------------------------------- subsamples

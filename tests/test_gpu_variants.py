@@ -1,6 +1,7 @@
 """Kernel variants selected by pv_set_option knobs give the same results (needs a B200).
 
-The persistent TMA-pipelined camera kernel (PV_OPT_CAM_PIPE, pv_pipe.cuh) runs when the
+The persistent TMA-pipelined camera kernels (PV_OPT_CAM_PIPE: 1 = k_cam_pipe, pv_pipe.cuh;
+2 = the warp-specialized k_cam_pipe2, pv_pipe2.cuh) run when the
 landmark blocks are small enough for one warp per camera (wpc == 1, the vlarge case);
 there it must reproduce k_cam bit for bit, and both must match the reference's golden
 step and 20-iteration cost trace (tests/golden/tiny_lm.npz) within the north_star's
@@ -37,7 +38,8 @@ def test_pipe_matches_k_cam(pv, stage):
     st = pv.ProjectiveState(z["cams"], z["lms"]) if stage == 1 else \
         pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"])
     outs = []
-    variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)])
+    variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
+                [(_lib.PV_OPT_CAM_PIPE, 2)])
     for knobs in variants:
         dp = _ctx(pv, z, knobs)
         info = dp.info()
@@ -62,10 +64,11 @@ def test_pipe_matches_k_cam(pv, stage):
         assert rel(a.landmark_update, z[key + "dl"]) <= tol
 
 
-def test_pipe_lm_trace_matches_reference(pv):
+@pytest.mark.parametrize("ver", [1, 2])
+def test_pipe_lm_trace_matches_reference(pv, ver):
     from paper_2405_05079_b200 import _lib
     z = golden("tiny_lm.npz")
-    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, 1)])
+    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, ver)])
     st = pv.ProjectiveState(z["cams"], z["lms"])
     _, trace = pv.lm_minimize(dp.problem, st, 1, pv.SolverConfig(max_outer_iterations=20),
                               dp=dp)
@@ -95,14 +98,17 @@ def test_pipe_long_work_lists_large(pv, stage):
     dp.damp(1e-4, stage == 2)
     assert dp.info()["warps_per_cam"] == 1 and dp.info()["blocks"] > 10
     out = []
-    for v in (0, 1):
+    for v in (0, 1, 2):
         dp.set_option(_lib.PV_OPT_CAM_PIPE, v)
+        dp.linearize(stage)
+        dp.damp(1e-4, stage == 2)
         order, trunc = dp.power_solve(4, 0.0)
         dx, dl = dp.step(stage)
         out.append((order, trunc, dx.copy(), dl.copy()))
-    assert out[0][0] == out[1][0] == 4 and out[0][1] == out[1][1]
-    np.testing.assert_array_equal(out[0][2], out[1][2])
-    np.testing.assert_array_equal(out[0][3], out[1][3])
+    for o in out[1:]:
+        assert out[0][0] == o[0] == 4 and out[0][1] == o[1]
+        np.testing.assert_array_equal(out[0][2], o[2])
+        np.testing.assert_array_equal(out[0][3], o[3])
 
 
 @pytest.mark.parametrize("slots", [0, 1])

@@ -33,6 +33,8 @@ for rnd in range(rounds):
     for i, var in enumerate(variants):
         for k, v in var:
             dp.set_option(k, v)
+        dp.linearize(stage)  # some knobs rebuild the work lists
+        dp.damp(1e-4, stage == 2)
         order, trunc = dp.power_solve(30, 0.01)
         dx = dp.step(stage)[0].copy()
         if ref is None:
