@@ -5,7 +5,7 @@ NVFLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -O3 --ex
 PKG := paper_2405_05079_b200
 LIB := $(PKG)/libpovar.so
 SRC := $(PKG)/csrc/povar.cu
-HDR := $(PKG)/csrc/pv_kernels.cuh $(PKG)/csrc/pv_device.cuh $(PKG)/csrc/pv_pcg.cuh $(PKG)/csrc/pv_pipe.cuh $(PKG)/csrc/pv_pipe2.cuh include/povar.h
+HDR := $(PKG)/csrc/pv_kernels.cuh $(PKG)/csrc/pv_device.cuh $(PKG)/csrc/pv_pcg.cuh $(PKG)/csrc/pv_pipe.cuh include/povar.h
 BALSRC := $(PKG)/csrc/pv_bal.cpp
 BALOBJ := build/pv_bal.o
 

@@ -93,8 +93,11 @@ enum {
                                   POSE_ONLY) reuses the reduced RHS -(b_p - W V+ b_l)      */
   PV_OPT_COST_CS = 12,         /* 1: pv_cost walks the camera-sorted segments (one camera load
                                   per warp segment); 0: landmark-task order                */
-  PV_OPT_BENCH_SPLIT = 13      /* diagnostic: pv_bench_terms times the W^T v passes (ms[0]) and
+  PV_OPT_BENCH_SPLIT = 13,     /* diagnostic: pv_bench_terms times the W^T v passes (ms[0]) and
                                   the W t passes (ms[1]) of all blocks on their own         */
+  PV_OPT_XM = 14               /* 1 (default): stage-1 pipelined camera passes stream x and m as
+                                  (x0 x1 x2 m0 | m1), 40 instead of 48 bytes per observation,
+                                  when every landmark has w = 1                             */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

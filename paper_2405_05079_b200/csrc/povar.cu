@@ -20,7 +20,6 @@
 #include "pv_kernels.cuh"
 #include "pv_pcg.cuh"
 #include "pv_pipe.cuh"
-#include "pv_pipe2.cuh"
 
 using namespace pv;
 
@@ -48,6 +47,7 @@ struct PvError : std::runtime_error {
   } while (0)
 
 inline int blocks_for(long long n, int per) { return (int)std::max(1LL, (n + per - 1) / per); }
+const double* const g_null_d = nullptr;
 
 }  // namespace
 
@@ -97,10 +97,8 @@ struct pv_ctx {
   int num_sms = 148;
   int wpc = 1;  // warps per camera in the camera kernels (from the mean segment size)
   // work lists of the persistent camera kernel (k_cam_pipe)
-  int pipe_W = 0;          // consumer warps the item lists were built for
-  int pipe_W_of[3] = {0, 0, 0};
+  int pipe_W = 0;
   int bench_split = 0;  // pv_bench_terms diagnostic (PV_OPT_BENCH_SPLIT)
-  int* d_pipe_ctr = nullptr;
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
@@ -108,7 +106,9 @@ struct pv_ctx {
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
   // state and solve buffers (device)
-  double *crec, *lrec, *lvr, *lbl, *ldl, *tlm, *tcam, *cs_x;
+  double *crec, *lrec, *lvr, *lbl, *ldl, *tlm, *tcam, *cs_x, *cs_xm;
+  double* d_cs_m1 = nullptr;  // m1 per camera-sorted observation (compact stage-1 stream)
+  bool xm_ok = false;         // cs_xm holds the current linearization point (stage 1, w == 1)
   double *lsys = nullptr, *tarr = nullptr, *sbuf = nullptr;
   double *cU, *cUd, *cUi, *cbp, *cx, *crhs, *ch, *cy, *cyr, *cUraw, *nrm, *ctmp, *scal;
   double* cpart = nullptr;
@@ -122,7 +122,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 0, 1, 1, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -290,6 +290,7 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->d_cs_kpos = c->alloc<int>((size_t)n_os + 128);
   c->d_lpos = c->alloc<int>((size_t)n_ls + 1);
   c->d_cs_m = c->alloc<double>(2 * ((size_t)n_os + 128));
+  c->d_cs_m1 = c->alloc<double>((size_t)n_os + 128);
   c->sync();  // host vectors go out of scope
   c->h_ls_cam = std::move(ls_cam);
   c->h_ls_lid = std::move(ls_lid);
@@ -341,37 +342,25 @@ static void ensure_cpart(pv_ctx* c) {
 // per-item overhead) and cut each (camera, block) segment into items of <= PCH
 // observations.  The W t list has >= 1 item per camera so that y is always written.
 static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
-  // consumer warps of the persistent grid: resident CTAs per SM x SMs x warps per CTA
-  // (k_cam_pipe: every warp; k_cam_pipe2: the consumer warps)
-  const int ver = c->tune.cam_pipe == 2 ? 2 : 1;
-  if (!c->pipe_W_of[ver]) {
+  if (!c->pipe_W) {
     int occ = 1 << 30;
-    auto occ_of = [&](const void* fn, int threads, int smem) {
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    auto occ_of = [&](const void* fn) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PIPE_SMEM));
       int o = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, PW * 32, PIPE_SMEM));
       occ = std::min(occ, o);
     };
-    if (ver == 2) {
-      occ_of((const void*)k_cam_pipe2<1, true, true>, P2T, PIPE2_SMEM);
-      occ_of((const void*)k_cam_pipe2<2, true, true>, P2T, PIPE2_SMEM);
-      occ_of((const void*)k_cam_pipe2<1, false, true>, P2T, PIPE2_SMEM);
-      occ_of((const void*)k_cam_pipe2<2, false, true>, P2T, PIPE2_SMEM);
-      occ_of((const void*)k_cam_pipe2<1, true, false>, P2T, PIPE2_SMEM);
-      occ_of((const void*)k_cam_pipe2<2, true, false>, P2T, PIPE2_SMEM);
-      c->pipe_W_of[ver] = std::max(1, occ) * c->num_sms * P2C;
-    } else {
-      occ_of((const void*)k_cam_pipe<1, true, true>, PW * 32, PIPE_SMEM);
-      occ_of((const void*)k_cam_pipe<2, true, true>, PW * 32, PIPE_SMEM);
-      occ_of((const void*)k_cam_pipe<1, false, true>, PW * 32, PIPE_SMEM);
-      occ_of((const void*)k_cam_pipe<2, false, true>, PW * 32, PIPE_SMEM);
-      occ_of((const void*)k_cam_pipe<1, true, false>, PW * 32, PIPE_SMEM);
-      occ_of((const void*)k_cam_pipe<2, true, false>, PW * 32, PIPE_SMEM);
-      c->pipe_W_of[ver] = std::max(1, occ) * c->num_sms * PW;
-    }
+    occ_of((const void*)k_cam_pipe<1, true, true, false>);
+    occ_of((const void*)k_cam_pipe<2, true, true, false>);
+    occ_of((const void*)k_cam_pipe<1, false, true, false>);
+    occ_of((const void*)k_cam_pipe<2, false, true, false>);
+    occ_of((const void*)k_cam_pipe<1, true, false, false>);
+    occ_of((const void*)k_cam_pipe<2, true, false, false>);
+    occ_of((const void*)k_cam_pipe<1, true, true, true>);
+    occ_of((const void*)k_cam_pipe<1, false, true, true>);
+    occ_of((const void*)k_cam_pipe<1, true, false, true>);
+    c->pipe_W = std::max(1, occ) * c->num_sms * PW;
   }
-  c->pipe_W = c->pipe_W_of[ver];
-  if (!c->d_pipe_ctr) c->d_pipe_ctr = c->alloc<int>(4);  // k_cam_pipe2's self-resetting counter
   const int B = c->n_blk, W = c->pipe_W;
   const int64_t np = c->n_p;
   constexpr int ITEM_COST = 24;  // observation-equivalents of one item's fixed overhead
@@ -591,7 +580,8 @@ static void build_blocks(pv_ctx* c) {
                      cudaMemcpyHostToDevice, c->stream));
   k_gather_m<<<blocks_for(n_os, 256), 256, 0, c->stream>>>(n_os, c->d_cs_pos, c->d_ls_m,
                                                            c->d_cs_m);
-  c->launched();
+  k_gather_m1<<<blocks_for(n_os, 256), 256, 0, c->stream>>>(n_os, c->d_cs_m, c->d_cs_m1);
+  c->launched(2);
   c->sync();
   c->blk_task = bt;
   c->n_blk = B;
@@ -616,6 +606,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->lvr = c->alloc<double>(nl * 8);
   // c->lsys, c->tarr: allocated by build_ktasks (warp-slot order)
   c->cs_x = c->alloc<double>(((size_t)c->n_os + 128) * 4);
+  c->cs_xm = c->alloc<double>(((size_t)c->n_os + 128) * 4);
   // c->sbuf: sized by build_ktasks (slot layout, padding lanes included)
   c->lbl = c->alloc<double>(nl * 4);
   c->ldl = c->alloc<double>(nl * 4);
@@ -683,7 +674,8 @@ template <int S>
 static int op_linearize(pv_ctx* c) {
   ++c->lin_id;
   CK(cudaMemsetAsync(c->flags, 0, F_COUNT * sizeof(int), c->stream));
-  k_build_csx<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x);
+  k_build_csx<S><<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->g, c->lrec, c->cs_x,
+                                                                   c->cs_xm, c->flags);
   if (!(S == 1 && c->lm_lin_fresh)) {
     if (c->tune.resolve_slots) {  // the lane-per-landmark slot kernels (same knob)
       const int ns = c->blk_ktask[c->n_blk];
@@ -712,6 +704,7 @@ static int op_linearize(pv_ctx* c) {
   c->sync();
   c->lin_stage = S;
   c->vp_cached = false;
+  c->xm_ok = S == 1 && !fl[F_XM_BAD];
   if (S == 2 && fl[F_INVALID_Z]) {
     c->lin_stage = 0;
     return PV_EDEGENERATE;
@@ -773,16 +766,15 @@ static void launch_cam_v(pv_ctx* c, const CamArgs& ca) {
 template <int S, bool HC, bool HA>
 static void launch_cam_pipe(pv_ctx* c, const CamArgs& ca) {
   PipeItems it{c->d_items, c->d_item_off, c->n_blk, c->pipe_W};
-  if (c->tune.cam_pipe == 2) {
-    k_cam_pipe2<S, HC, HA><<<c->pipe_W / P2C, P2T, PIPE2_SMEM, c->stream>>>(
-        c->g, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
-        ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi, c->d_pipe_ctr);
-    c->launched();
-    return;
+  if (S == 1 && c->xm_ok && c->tune.xm) {  // compact stage-1 stream (x0 x1 x2 m0 | m1)
+    k_cam_pipe<S, HC, HA, true><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
+        c->g, it, c->crec, c->cs_xm, c->d_cs_m1, c->tarr, c->sbuf, c->cy, c->ctl, c->coef,
+        c->tune, ca.c_lo, ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi);
+  } else {
+    k_cam_pipe<S, HC, HA, false><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
+        c->g, it, c->crec, c->cs_x, g_null_d, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune,
+        ca.c_lo, ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi);
   }
-  k_cam_pipe<S, HC, HA><<<c->pipe_W / PW, PW * 32, PIPE_SMEM, c->stream>>>(
-      c->g, it, c->crec, c->cs_x, c->tarr, c->sbuf, c->cy, c->ctl, c->coef, c->tune, ca.c_lo,
-      ca.first_c, ca.a_lo, ca.check_stop, ca.disc_lo, ca.disc_hi);
   c->launched();
 }
 
@@ -1262,6 +1254,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_RHS_REUSE:
       c->tune.rhs_reuse = value ? 1 : 0;
       break;
+    case PV_OPT_XM:
+      c->tune.xm = value ? 1 : 0;
+      break;
     case PV_OPT_BENCH_SPLIT:
       c->bench_split = value ? 1 : 0;
       break;
@@ -1271,13 +1266,8 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_SPLIT_LAST:
       c->tune.split_last = value ? 1 : 0;
       break;
-    case PV_OPT_CAM_PIPE:  // 0: k_cam, 1: k_cam_pipe, 2: warp-specialized k_cam_pipe2
-      if (value < 0 || value > 2) throw PvError(PV_EINVAL, "PV_OPT_CAM_PIPE must be 0, 1 or 2");
-      if ((value == 2) != (c->tune.cam_pipe == 2)) {
-        c->tune.cam_pipe = (int)value;
-        build_blocks(c);  // the item lists depend on the consumer-warp count
-      }
-      c->tune.cam_pipe = (int)value;
+    case PV_OPT_CAM_PIPE:
+      c->tune.cam_pipe = value ? 1 : 0;
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
@@ -1609,20 +1599,6 @@ int pv_bench_terms(pv_ctx* c, int stage, int n, float* ms) {
   API_END(c)
 }
 
-#ifdef PV_PIPE2_TIMING
-// diagnostic build only: start / end globaltimer and item count of every consumer warp of
-// the last k_cam_pipe2 launch
-int pv_debug_pipe2_times(pv_ctx* c, unsigned long long* t, int* items, int* n,
-                         unsigned long long* entry) {
-  API_BEGIN(c)
-  CK(cudaStreamSynchronize(c->stream));
-  *n = c->pipe_W;
-  CK(cudaMemcpyFromSymbol(entry, pv::g_pipe2_entry, sizeof(unsigned long long) * (c->pipe_W / P2C)));
-  CK(cudaMemcpyFromSymbol(t, pv::g_pipe2_t, sizeof(unsigned long long) * 2 * c->pipe_W));
-  CK(cudaMemcpyFromSymbol(items, pv::g_pipe2_items, sizeof(int) * c->pipe_W));
-  API_END(c)
-}
-#endif
 
 int pv_debug_get(pv_ctx* c, int which, double* out) {
   API_BEGIN(c)

@@ -34,7 +34,7 @@ struct Tune {
   int pol_t;       // landmark vectors t (gathered)
   int pol_s;       // per-observation partials s (scattered / streamed)
   int discard_s;   // drop consumed s lines from L2 (no write-back)
-  int reserved7;     // (option 7: a removed camera-kernel variant)
+  int xm;            // 1: stage-1 pipelined passes stream the compact (x0 x1 x2 m0 | m1) layout
   int cam_pipe;      // single-block camera passes: persistent TMA-pipelined k_cam_pipe
   int resolve_slots; // landmark re-solve: one lane per landmark over the k-bucketed slots
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
@@ -43,7 +43,7 @@ struct Tune {
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
-       F_N_FALLBACK = 5, F_SINGULAR_M = 6, F_SINGULAR_M2 = 7, F_COUNT = 8 };
+       F_N_FALLBACK = 5, F_SINGULAR_M = 6, F_SINGULAR_M2 = 7, F_XM_BAD = 8, F_COUNT = 9 };
 
 struct Graph {
   int n_p, n_l, n_o;
@@ -724,11 +724,29 @@ __global__ void k_gather_m(int n_o, const int* __restrict__ cs_pos, const double
   reinterpret_cast<double2*>(cs_m)[o] = reinterpret_cast<const double2*>(ls_m)[__ldg(cs_pos + o)];
 }
 
-// camera-sorted copy of the landmark coordinates (once per linearization point)
-__global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __restrict__ cs_x) {
+// camera-sorted copy of the landmark coordinates (once per linearization point).  Stage 1
+// also writes the compact stream of the pipelined camera passes, xm = (x0, x1, x2, m0) with
+// m1 in its own array (cs_m1): the landmark's w = 1 is not streamed (40 instead of 48 bytes
+// of x and m per observation and pass).  A landmark with w != 1 sets F_XM_BAD and the term
+// kernels keep the full stream.
+template <int STAGE>
+__global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __restrict__ cs_x,
+                            double* __restrict__ cs_xm, int* __restrict__ flags) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= g.n_o) return;
-  st4(cs_x + 4 * (size_t)o, ldg4(lrec + (size_t)__ldg(g.cs_lm + o) * LREC));
+  const double4 x = ldg4(lrec + (size_t)__ldg(g.cs_lm + o) * LREC);
+  st4(cs_x + 4 * (size_t)o, x);
+  if (STAGE == 1) {
+    st4(cs_xm + 4 * (size_t)o, make_double4(x.x, x.y, x.z, __ldg(g.cs_m + 2 * (size_t)o)));
+    if (x.w != 1.0) atomicOr(flags + F_XM_BAD, 1);
+  }
+}
+
+// m1 of every block-major camera-sorted observation (once per re-blocking)
+__global__ void k_gather_m1(int n_o, const double* __restrict__ cs_m, double* __restrict__ cs_m1) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n_o) return;
+  cs_m1[o] = cs_m[2 * (size_t)o + 1];
 }
 
 // ---------------------------------------------------------------------------

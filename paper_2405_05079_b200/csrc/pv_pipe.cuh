@@ -111,10 +111,14 @@ struct PipeItems {
   int B, W;
 };
 
-template <int STAGE, bool HC, bool HA>
+// XM (stage 1, every landmark w = 1): cs_x is the compact stream xm = (x0, x1, x2, m0) and
+// cs_m1 holds m1 -- 40 instead of 48 bytes of x and m per observation (k_build_csx); x.w = 1
+// and m are rebuilt in registers, so both layouts give the same bits.
+template <int STAGE, bool HC, bool HA, bool XM>
 __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, PipeItems it,
                                                       const double* __restrict__ crec,
                                                       const double* __restrict__ cs_x,
+                                                      const double* __restrict__ cs_m1,
                                                       const double* __restrict__ tarr,
                                                       double* __restrict__ sbuf,
                                                       double* __restrict__ cy,
@@ -178,11 +182,16 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
         const int* ids = (fl & PF_HA) ? g.cs_pos : g.cs_kpos;
         const int i0 = o & ~3;
         const int i1 = (o + n + 3) & ~3;
-        const unsigned bx = (unsigned)n * 32u, bm = (unsigned)n * 16u,
+        // XM: m1 copied from the 16-byte aligned o & ~1 (one extra leading double)
+        const unsigned bx = (unsigned)n * 32u,
+                       bm = XM ? (unsigned)(((o + n + 1) & ~1) - (o & ~1)) * 8u : (unsigned)n * 16u,
                        bi = (unsigned)(i1 - i0) * 4u;
         mbar_arrive_tx(bars + s, bx + bm + bi + 192u);
         bulk_g2s(slot + PX_OFF, cs_x + 4 * (size_t)o, bx, bars + s, pf);
-        bulk_g2s(slot + PM_OFF, g.cs_m + 2 * (size_t)o, bm, bars + s, pf);
+        if (XM)
+          bulk_g2s(slot + PM_OFF, cs_m1 + (o & ~1), bm, bars + s, pf);
+        else
+          bulk_g2s(slot + PM_OFF, g.cs_m + 2 * (size_t)o, bm, bars + s, pf);
         bulk_g2s(slot + PI_OFF, ids + i0, bi, bars + s, pf);
         bulk_g2s(slot + PC_OFF, crec + (size_t)cam * CREC, 192u, bars + s, pt);
       } else {
@@ -238,6 +247,17 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     const double4* cr = reinterpret_cast<const double4*>(slot + PC_OFF);
     const double4* sx = reinterpret_cast<const double4*>(slot + PX_OFF);
     const double2* sm = reinterpret_cast<const double2*>(slot + PM_OFF);
+    const double* sm1 = reinterpret_cast<const double*>(slot + PM_OFF) + (o0 & 1);
+    // observation q's x (w = 1 rebuilt under XM) and m
+    auto xm_at = [&](int q, double4& X, double2& m) {
+      X = sx[q];
+      if (XM) {
+        m = make_double2(X.w, sm1[q]);
+        X.w = 1.0;
+      } else {
+        m = sm[q];
+      }
+    };
     if (!(fl & PF_HA)) {
       if (HC) {
         if (n > 0) {
@@ -247,8 +267,9 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
           for (int r = 0; r < (PCH + 31) / 32; ++r) {
             const int q = lane + 32 * r;
             if (q >= n) continue;
-            const double4 X = sx[q];
-            const double2 m = sm[q];
+            double4 X;
+            double2 m;
+            xm_at(q, X, m);
             const double4 T = tq[q];
             const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
             double sg[3];
@@ -280,8 +301,9 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
       for (int r = 0; r < (PCH + 31) / 32; ++r) {
         const int q = lane + 32 * r;
         if (q >= n) continue;
-        const double4 X = sx[q];
-        const double2 m = sm[q];
+        double4 X;
+        double2 m;
+        xm_at(q, X, m);
         const int pos = si[q];
         const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
         double f0, f1, f2;

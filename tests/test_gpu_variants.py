@@ -1,7 +1,6 @@
 """Kernel variants selected by pv_set_option knobs give the same results (needs a B200).
 
-The persistent TMA-pipelined camera kernels (PV_OPT_CAM_PIPE: 1 = k_cam_pipe, pv_pipe.cuh;
-2 = the warp-specialized k_cam_pipe2, pv_pipe2.cuh) run when the
+The persistent TMA-pipelined camera kernel (PV_OPT_CAM_PIPE, pv_pipe.cuh) runs when the
 landmark blocks are small enough for one warp per camera (wpc == 1, the vlarge case);
 there it must reproduce k_cam bit for bit, and both must match the reference's golden
 step and 20-iteration cost trace (tests/golden/tiny_lm.npz) within the north_star's
@@ -39,7 +38,7 @@ def test_pipe_matches_k_cam(pv, stage):
         pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"])
     outs = []
     variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
-                [(_lib.PV_OPT_CAM_PIPE, 2)])
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_XM, 0)])
     for knobs in variants:
         dp = _ctx(pv, z, knobs)
         info = dp.info()
@@ -64,11 +63,29 @@ def test_pipe_matches_k_cam(pv, stage):
         assert rel(a.landmark_update, z[key + "dl"]) <= tol
 
 
-@pytest.mark.parametrize("ver", [1, 2])
-def test_pipe_lm_trace_matches_reference(pv, ver):
+def test_compact_stream_falls_back_when_w_is_not_one(pv):
+    """The compact stage-1 stream (PV_OPT_XM) drops the landmark's w = 1; a stage-1 state
+    whose landmarks do not all have w = 1 (the reference uses the full 4-vector,
+    objective.py:68-110) must take the full stream and still match k_cam bit for bit."""
     from paper_2405_05079_b200 import _lib
     z = golden("tiny_lm.npz")
-    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, ver)])
+    lms = np.array(z["lms"])
+    lms[::7, 3] = 1.5
+    st = pv.ProjectiveState(z["cams"], lms)
+    outs = []
+    for knobs in ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)]):
+        dp = _ctx(pv, z, knobs)
+        sysm = pv.assemble_system(dp.problem, st, 1, 1e-4, "pose_only", dp=dp)
+        outs.append(pv.power_schur_solve(sysm, pv.SolverConfig()))
+    assert outs[0].power_order_used == outs[1].power_order_used
+    np.testing.assert_array_equal(outs[0].pose_update, outs[1].pose_update)
+    np.testing.assert_array_equal(outs[0].landmark_update, outs[1].landmark_update)
+
+
+def test_pipe_lm_trace_matches_reference(pv):
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, 1)])
     st = pv.ProjectiveState(z["cams"], z["lms"])
     _, trace = pv.lm_minimize(dp.problem, st, 1, pv.SolverConfig(max_outer_iterations=20),
                               dp=dp)
@@ -98,7 +115,7 @@ def test_pipe_long_work_lists_large(pv, stage):
     dp.damp(1e-4, stage == 2)
     assert dp.info()["warps_per_cam"] == 1 and dp.info()["blocks"] > 10
     out = []
-    for v in (0, 1, 2):
+    for v in (0, 1):
         dp.set_option(_lib.PV_OPT_CAM_PIPE, v)
         dp.linearize(stage)
         dp.damp(1e-4, stage == 2)
