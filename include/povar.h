@@ -104,6 +104,12 @@ enum {
  * host broadcasts it (torch.distributed store) before pv_create. */
 int pv_nccl_unique_id(unsigned char out[128]);
 
+/* In-process loopback "communicator" for testing the sharded path on ONE device: returns an
+ * id to pass as nccl_id to pv_create for each of `world` contexts (ranks) of this process on
+ * the same device, each driven by its own host thread.  Allreduces become rank-ordered
+ * device sums between host barriers (bit-identical replicas, as with NCCL). */
+int pv_loopback_id(int world, unsigned char out[128]);
+
 /* Upload the observation graph once: landmark-CSR order, camera-sorted
  * permutation, warp work units; replaces the per-iteration landmark_order +
  * _group_blocks bucketing (objective.py:237-248, normal_eq.py:92-106).

@@ -35,6 +35,7 @@ _D = ctypes.POINTER(ctypes.c_double)
 _I64 = ctypes.POINTER(ctypes.c_int64)
 SIGNATURES = [
     ("pv_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("pv_loopback_id", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p]),
     ("pv_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                  _I64, _I64, _D, ctypes.c_int64, ctypes.c_int64,

@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -48,6 +50,53 @@ struct PvError : std::runtime_error {
 
 inline int blocks_for(long long n, int per) { return (int)std::max(1LL, (n + per - 1) / per); }
 const double* const g_null_d = nullptr;
+
+// In-process loopback communicator: W contexts of one process on one device, one host
+// thread per rank, standing in for NCCL so the sharded code path (split camera kernels,
+// replicated epilogue, collective flags) runs and is tested on a single GPU.  An allreduce
+// is two host barriers around device work: every rank records "my buffer is ready", then
+// sums ALL ranks' buffers in rank order into a scratch buffer (same-device reads ordered by
+// cudaStreamWaitEvent), records "read done", and after the second barrier copies the sum
+// back once every rank has read its buffer.  Every rank adds the same values in the same
+// order, so the replicas are bit-identical, as with NCCL.
+struct LoopGroup {
+  static constexpr uint64_t MAGIC = 0x4b4250504f4f4c50ull;  // "PLOOPPBK"
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const void*> bufs;
+  std::vector<cudaEvent_t> ready, done;
+  int members = 0;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+__global__ void k_loop_sum(int world, const double* const* bufs, size_t n, double* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = bufs[0][i];
+    for (int q = 1; q < world; ++q) s += bufs[q][i];
+    out[i] = s;
+  }
+}
+__global__ void k_loop_max(int world, const int* const* bufs, int n, int* out) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  int s = bufs[0][i];
+  for (int q = 1; q < world; ++q) s = max(s, bufs[q][i]);
+  out[i] = s;
+}
 
 }  // namespace
 
@@ -148,12 +197,44 @@ struct pv_ctx {
 
   // the collective (sharded) code path: world > 1, or forced on one GPU with a
   // 1-rank NCCL communicator to exercise the split kernels + NCCL calls
-  bool collective() const { return comm != nullptr; }
+  bool collective() const { return comm != nullptr || loop != nullptr; }
   void allreduce(double* p, size_t n) {
     if (comm) NK(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, stream));
+    if (loop) loop_allreduce(p, n, false);
   }
   void allreduce_flags() {
     if (comm) NK(ncclAllReduce(flags, flags, F_COUNT, ncclInt32, ncclMax, comm, stream));
+    if (loop) loop_allreduce(flags, F_COUNT, true);
+  }
+  // loopback communicator (LoopGroup): one host thread per rank
+  LoopGroup* loop = nullptr;
+  void* loop_tmp = nullptr;     // rank-order sum (n_p * 144 doubles)
+  void** loop_ptrs = nullptr;   // device array of the ranks' buffer pointers
+  void loop_allreduce(void* p, size_t n, bool is_flags) {
+    LoopGroup& G = *loop;
+    G.bufs[rank] = p;
+    CK(cudaEventRecord(G.ready[rank], stream));
+    G.barrier();  // every rank's buffer pointer and ready event are posted
+    for (int q = 0; q < world; ++q)
+      if (q != rank) CK(cudaStreamWaitEvent(stream, G.ready[q], 0));
+    CK(cudaMemcpyAsync(loop_ptrs, G.bufs.data(), sizeof(void*) * world, cudaMemcpyHostToDevice,
+                       stream));
+    if (is_flags)
+      k_loop_max<<<1, 32, 0, stream>>>(world, (const int* const*)loop_ptrs, (int)n,
+                                       (int*)loop_tmp);
+    else
+      k_loop_sum<<<(int)std::min<size_t>(1024, (n + 255) / 256), 256, 0, stream>>>(
+          world, (const double* const*)loop_ptrs, n, (double*)loop_tmp);
+    launched();
+    CK(cudaEventRecord(G.done[rank], stream));
+    CK(cudaStreamSynchronize(stream));  // the host-side pointer array copy is consumed
+    G.barrier();  // every rank has enqueued (and finished) its reads
+    for (int q = 0; q < world; ++q)
+      if (q != rank) CK(cudaStreamWaitEvent(stream, G.done[q], 0));
+    CK(cudaMemcpyAsync(p, loop_tmp, n * (is_flags ? sizeof(int) : sizeof(double)),
+                       cudaMemcpyDeviceToDevice, stream));
+    // (no third barrier: a rank re-records its events only after the next collective's first
+    // barrier, i.e. after every rank has enqueued its waits on this collective's events)
   }
   void sync() { CK(cudaStreamSynchronize(stream)); }
 
@@ -919,13 +1000,18 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     mark_rhs<S>(c);
   }
   c->check_launch();
-  // K5 + K6 terms with a one-term lookahead on the device stop flag
+  // K5 + K6 terms with a one-term lookahead on the device stop flag.  The decision to stop
+  // launching must be the same on every rank (each launch of a term holds collectives):
+  // after term i-1 is known complete, stop only on a stop taken AT a term <= i-1 -- a faster
+  // rank may already see the stop of the in-flight term i, and must not act on it earlier
+  // than the others (the loopback test caught exactly that divergence).
   for (int i = 1; i <= max_order; ++i) {
     launch_term<S>(c, i, thr);
     CK(cudaEventRecord(c->ev[i & 1], c->stream));
     if (i >= 2) {
       CK(cudaEventSynchronize(c->ev[(i - 1) & 1]));
-      if (((volatile PowerCtl*)c->host_ctl)->stopped) break;
+      const volatile PowerCtl* h = c->host_ctl;
+      if (h->stopped && h->term <= i - 1) break;
     }
   }
   c->check_launch();
@@ -992,8 +1078,10 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   c->launched();
   c->check_launch();
   c->sync();
-  // iterations with a one-iteration look-ahead on the device stop flag
-  for (int it = 1; it <= max_it && !((volatile PowerCtl*)c->host_ctl)->stopped; ++it) {
+  // iterations with a one-iteration look-ahead on the device stop flag; as in op_power the
+  // host acts only on a stop taken at an iteration known complete (rank-consistent)
+  const bool stopped0 = ((volatile PowerCtl*)c->host_ctl)->stopped != 0;  // after the sync
+  for (int it = 1; it <= max_it && !stopped0; ++it) {
     launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 1));
     for (int b = 0; b < B; ++b) {
       launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
@@ -1012,7 +1100,8 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
     CK(cudaEventRecord(c->ev[it & 1], c->stream));
     if (it >= 2) {
       CK(cudaEventSynchronize(c->ev[(it - 1) & 1]));
-      if (((volatile PowerCtl*)c->host_ctl)->stopped) break;
+      const volatile PowerCtl* h = c->host_ctl;
+      if (h->stopped && h->order <= it - 1) break;
     }
   }
   c->check_launch();
@@ -1102,6 +1191,20 @@ static void op_accept(pv_ctx* c, bool lm_lin_fresh = false) {
 
 extern "C" {
 
+int pv_loopback_id(int world, unsigned char out[128]) {
+  if (world < 1 || !out) return PV_EINVAL;
+  LoopGroup* G = new LoopGroup();  // lives for the process (a test / single-node utility)
+  G->world = world;
+  G->bufs.assign(world, nullptr);
+  G->ready.assign(world, nullptr);
+  G->done.assign(world, nullptr);
+  std::memset(out, 0, 128);
+  const uint64_t magic = LoopGroup::MAGIC;
+  std::memcpy(out, &magic, sizeof(magic));
+  std::memcpy(out + 8, &G, sizeof(G));
+  return PV_OK;
+}
+
 int pv_nccl_unique_id(unsigned char out[128]) {
   ncclUniqueId id;
   if (ncclGetUniqueId(&id) != ncclSuccess) return PV_ENCCL;
@@ -1159,9 +1262,28 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
     for (auto& e : c->tev) CK(cudaEventCreate(&e));
     if (world > 1) {
       if (!nccl_id) throw PvError(PV_EINVAL, "nccl id required for world > 1");
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
-      NK(ncclCommInitRank(&c->comm, world, id, rank));
+      uint64_t magic = 0;
+      std::memcpy(&magic, nccl_id, sizeof(magic));
+      if (magic == LoopGroup::MAGIC) {  // in-process loopback (pv_loopback_id)
+        LoopGroup* G = nullptr;
+        std::memcpy(&G, nccl_id + 8, sizeof(G));
+        if (!G || G->world != world) throw PvError(PV_EINVAL, "loopback group size mismatch");
+        c->loop = G;
+        {
+          std::lock_guard<std::mutex> lk(G->m);
+          if (!G->ready[rank]) {
+            CK(cudaEventCreateWithFlags(&G->ready[rank], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&G->done[rank], cudaEventDisableTiming));
+          }
+          ++G->members;
+        }
+        c->loop_tmp = c->alloc<double>((size_t)std::max<int64_t>(n_cameras, 1) * 144);
+        c->loop_ptrs = c->alloc<void*>(world);
+      } else {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        NK(ncclCommInitRank(&c->comm, world, id, rank));
+      }
     }
     build_graph(c, cam_idx, lm_idx, meas, lm_begin, lm_end);
     build_blocks(c);

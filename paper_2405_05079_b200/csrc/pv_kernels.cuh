@@ -504,12 +504,15 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
     c.xnorm = XN;
     c.tnorm = TN;
     *ctl = c;
-    host_ctl->stopped = c.stopped;
+    // the host's look-ahead loop reads `stopped`, then `term`: publish term first, so a rank
+    // never sees the stop without the term that took it (povar.cu op_power)
     host_ctl->order = c.order;
     host_ctl->term = c.term;
     host_ctl->trunc = c.trunc;
     host_ctl->xnorm = c.xnorm;
     host_ctl->tnorm = c.tnorm;
+    __threadfence_system();
+    host_ctl->stopped = c.stopped;
     __threadfence_system();
     *ticket = 0u;
   }

@@ -346,10 +346,12 @@ __device__ __forceinline__ void store_camera_vector(double* __restrict__ crec,
 __device__ __forceinline__ void publish(PowerCtl* ctl, volatile PowerCtl* host_ctl,
                                         const PowerCtl& c) {
   *ctl = c;
-  host_ctl->stopped = c.stopped;
+  // `order` (the iteration that stopped) before `stopped`: see op_pcg's look-ahead loop
   host_ctl->order = c.order;
   host_ctl->pad = c.pad;
   host_ctl->trunc = c.trunc;
+  __threadfence_system();
+  host_ctl->stopped = c.stopped;
   __threadfence_system();
 }
 

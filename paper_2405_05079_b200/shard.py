@@ -61,3 +61,26 @@ def broadcast_nccl_id(rank: int, world: int) -> bytes:
         obj = [buf]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+def loopback_id(world: int) -> bytes:
+    """An in-process loopback communicator for ``world`` contexts on ONE device, each driven
+    by its own host thread (``pv_loopback_id``): the sharded code path -- split camera
+    kernels, replicated epilogue, collective flags -- without a multi-GPU node."""
+    import ctypes
+
+    from . import _lib
+    raw = ctypes.create_string_buffer(128)
+    _lib.check(_lib.load().pv_loopback_id(int(world), raw))
+    return raw.raw
+
+
+def merge_states(states, plan):
+    """Whole-problem state from per-rank results: the (replicated) cameras of rank 0 and
+    each rank's own landmark range [begin, end) (a rank's ``get_state`` only updates the
+    landmarks it owns)."""
+    from .types import ProjectiveState
+    lms = np.array(states[0].landmarks, copy=True)
+    for st, (b, e) in zip(states, plan):
+        lms[b:e] = st.landmarks[b:e]
+    return ProjectiveState(states[0].cameras, lms)

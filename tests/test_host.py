@@ -191,3 +191,27 @@ def test_householder_bases_match_reference_convention():
                                             ref.landmark_bases)
     with pytest.raises(ValueError):
         solver._check_bases(st, other)
+
+
+def test_merge_states_and_loopback_id():
+    """shard.merge_states: replicated cameras of rank 0 + each rank's own landmark range;
+    pv_loopback_id (host-only) returns a 128-byte id tagged as an in-process group."""
+    from paper_2405_05079_b200 import shard
+    from paper_2405_05079_b200.types import ProjectiveState
+    rng = np.random.default_rng(3)
+    cams = rng.standard_normal((4, 3, 4))
+    base = rng.standard_normal((10, 4))
+    plan = [(0, 3), (3, 7), (7, 10)]
+    states = []
+    for r, (b, e) in enumerate(plan):
+        lms = base.copy()
+        lms[b:e] += r + 1.0
+        states.append(ProjectiveState(cams, lms))
+    merged = shard.merge_states(states, plan)
+    want = base.copy()
+    for r, (b, e) in enumerate(plan):
+        want[b:e] += r + 1.0
+    np.testing.assert_array_equal(merged.landmarks, want)
+    np.testing.assert_array_equal(merged.cameras, cams)
+    lid = shard.loopback_id(3)
+    assert len(lid) == 128 and lid[:8] == (0x4b4250504f4f4c50).to_bytes(8, "little")
