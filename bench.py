@@ -115,12 +115,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def term_bytes(n_p, n_l, n_o, stage=1, x_bytes=32):
+def term_bytes(n_p, n_l, n_o, stage=1, xm_bytes=48):
     """Bytes of one power-series term per kernel group.
 
     ``dram``: what the declared layout must move between HBM and the SMs per term.
-    The camera passes stream the camera-sorted x (``x_bytes``), m (16) and one int32
-    id (4) twice -- once for W t, once for W^T v -- plus per camera the 192-byte record
+    The camera passes stream the camera-sorted x and m (``xm_bytes``: 32 + 16, or 40 with
+    the compact stage-1 stream of PV_OPT_XM) and one int32 id (4) twice -- once for W t, once for W^T v -- plus per camera the 192-byte record
     per pass and y (96); the landmark reduces read each landmark's V+ record (64) and
     its work-slot entry (16; stage 2 also x, 32).  ``l2``: the transposes that the
     landmark blocking keeps in the persisting L2 by design -- the partials s (written
@@ -128,7 +128,7 @@ def term_bytes(n_p, n_l, n_o, stage=1, x_bytes=32):
     observation).  ``r1_term``: the reference's own layout (W stored, SURVEY section
     8(d)), for the north_star's roofline figure.
     """
-    cam = 2 * (x_bytes + 16 + 4) * n_o + (2 * 192 + 96) * n_p
+    cam = 2 * (xm_bytes + 4) * n_o + (2 * 192 + 96) * n_p
     lmr = (80 if stage == 1 else 112) * n_l
     l2 = {"cam": 32 * n_o + 32 * n_o, "lm_reduce": 32 * n_o + 32 * n_l}
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
@@ -316,7 +316,7 @@ def main():
     def start_run():
         dp.set_state(state0)
         run.update(f=dp.cost(1), lam=scfg.initial_lambda, linearized=False, orders=[],
-                   marks=[])
+                   marks=[], solve={})
 
     def lm_iteration(timed=False):
         # solver.lm_minimize's iteration: a rejected step leaves the state unchanged, so its
@@ -334,6 +334,10 @@ def main():
         run["orders"].append(order)
         if timed:
             m.append(ev())
+            inf = dp.info()
+            for k in ("solve_rhs_us", "solve_terms_us", "solve_backsub_us",
+                      "solve_terms_launched"):
+                run["solve"][k] = run["solve"].get(k, 0) + inf[k]
         ok = dp.trial(1)
         ft = dp.cost(1, trial=True) if ok else math.inf
         if timed:
@@ -373,6 +377,12 @@ def main():
         for k, a, b in zip(ops, m, m[1:]):
             breakdown[k] += a.elapsed_time(b) / args.steps
     breakdown = {k: round(max_over_ranks(v), 4) for k, v in breakdown.items()}
+    # the power solve split (device time inside pv_power_solve, povar.cu op_power)
+    breakdown.update({
+        "solve_rhs": round(run["solve"]["solve_rhs_us"] / 1e3 / args.steps, 4),
+        "solve_terms": round(run["solve"]["solve_terms_us"] / 1e3 / args.steps, 4),
+        "solve_backsub": round(run["solve"]["solve_backsub_us"] / 1e3 / args.steps, 4),
+        "terms_launched_per_step": run["solve"]["solve_terms_launched"] / args.steps})
 
     # ---- S'.v terms and per-kernel roofline (at the state after iteration K) ---------
     dp.linearize(1)
@@ -389,7 +399,7 @@ def main():
 
     def term_report(kt, stage):
         tb = term_bytes(n_p, loc["n_l_local"], loc["n_o_local"], stage,
-                        x_bytes=loc.get("x_bytes") or 32)
+                        xm_bytes=loc["xm_bytes"] if stage == 1 else 48)
         kern = {}
         for name, key, tkey in (("k_lm_reduce", "lm_reduce", "lm_reduce_ms"),
                                 (cam_name, "cam", "cam_ms")):

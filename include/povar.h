@@ -68,7 +68,14 @@ enum {
   PV_INFO_CHUNKS = 4, PV_INFO_LAUNCHES = 5, PV_INFO_RANK = 6, PV_INFO_WORLD = 7,
   PV_INFO_DEVICE_BYTES = 8, PV_INFO_NL_GLOBAL = 9, PV_INFO_RESOLVE_FALLBACKS = 10,
   PV_INFO_BLOCKS = 11, PV_INFO_PERSIST_L2 = 12, PV_INFO_WARPS_PER_CAM = 13,
-  PV_INFO_COUNT = 16
+  /* last pv_power_solve, device microseconds (CUDA events): reduced RHS + t_0, the term
+   * loop, the back-substitution; terms launched (incl. the look-ahead one) */
+  PV_INFO_SOLVE_RHS_US = 14, PV_INFO_SOLVE_TERMS_US = 15, PV_INFO_SOLVE_BACKSUB_US = 16,
+  PV_INFO_SOLVE_TERMS_LAUNCHED = 17,
+  /* bytes of x and m streamed per observation by a stage-1 camera pass (48, or 40 with the
+   * compact stream of PV_OPT_XM) */
+  PV_INFO_XM_BYTES = 18,
+  PV_INFO_COUNT = 24
 };
 
 /* tuning knobs of the term kernels (pv_set_option); results do not depend on them */
@@ -95,9 +102,12 @@ enum {
                                   per warp segment); 0: landmark-task order                */
   PV_OPT_BENCH_SPLIT = 13,     /* diagnostic: pv_bench_terms times the W^T v passes (ms[0]) and
                                   the W t passes (ms[1]) of all blocks on their own         */
-  PV_OPT_XM = 14               /* 1 (default): stage-1 pipelined camera passes stream x and m as
+  PV_OPT_XM = 14,              /* 1 (default): stage-1 pipelined camera passes stream x and m as
                                   (x0 x1 x2 m0 | m1), 40 instead of 48 bytes per observation,
                                   when every landmark has w = 1                             */
+  PV_OPT_GRAPH = 15            /* 1 (default): the power-series term loop runs as one CUDA graph
+                                  (WHILE conditional node, stop test on the device); 0: host
+                                  loop with a one-term look-ahead                            */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

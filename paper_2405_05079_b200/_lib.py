@@ -22,12 +22,13 @@ PV_CURRENT, PV_TRIAL = 0, 1
  PV_DBG_RHS, PV_DBG_X, PV_DBG_DL, PV_DBG_ULIN, PV_DBG_SDIAG, PV_DBG_MINV) = range(14)
 INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
                "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2",
-               "warps_per_cam")
-PV_INFO_COUNT = 16
+               "warps_per_cam", "solve_rhs_us", "solve_terms_us", "solve_backsub_us",
+               "solve_terms_launched", "xm_bytes")
+PV_INFO_COUNT = 24
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
  PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, _PV_OPT_RESERVED7, PV_OPT_CAM_PIPE,
  PV_OPT_RESOLVE_SLOTS, PV_OPT_SPLIT_LAST, PV_OPT_RHS_REUSE, PV_OPT_COST_CS,
- PV_OPT_BENCH_SPLIT, PV_OPT_XM) = range(15)
+ PV_OPT_BENCH_SPLIT, PV_OPT_XM, PV_OPT_GRAPH) = range(16)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
 _P = ctypes.c_void_p

@@ -100,6 +100,17 @@ __global__ void k_loop_max(int world, const int* const* bufs, int n, int* out) {
 
 }  // namespace
 
+// a captured term loop (term_graph) and the configuration it was captured for
+struct TermGraph {
+  int stage = 0, max_order = 0, n_blk = 0, wpc = 0, xm = 0;
+  double thr = 0.0;
+  Tune tune{};
+  bool coll = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long body_launches = 0;
+};
+
 struct pv_ctx {
   int device = 0, rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -148,6 +159,9 @@ struct pv_ctx {
   // work lists of the persistent camera kernel (k_cam_pipe)
   int pipe_W = 0;
   int bench_split = 0;  // pv_bench_terms diagnostic (PV_OPT_BENCH_SPLIT)
+  int64_t solve_us[3] = {0, 0, 0};  // last power solve: RHS, terms, back-substitution
+  int64_t solve_terms_launched = 0;
+  TermGraph tgraph;
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
@@ -171,7 +185,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -896,7 +910,7 @@ static void launch_lm_reduce(pv_ctx* c, int b_lo, int b_hi, int check_stop) {
 
 static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int term,
                         double thr, int check_stop) {
-  CamArgs a;
+  CamArgs a{};
   a.c_lo = c_lo;
   a.c_hi = c_hi;
   a.first_c = first_c;
@@ -916,7 +930,12 @@ static CamArgs cam_args(int c_lo, int c_hi, int first_c, int a_lo, int a_hi, int
 // finish y over blocks [c_lo, c_hi) (if any), the epilogue, and the gather of block 0
 template <int S, int EP>
 static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term, double thr,
-                            int check_stop) {
+                            int check_stop, unsigned long long cond = 0, int max_order = 0) {
+  auto ep_args = [&](CamArgs a) {  // the epilogue launch carries the term-graph condition
+    a.cond = cond;
+    a.max_order = max_order;
+    return a;
+  };
   if (!c->collective() && c->tune.split_last && c->wpc == 1) {
     // one warp per camera: the W t pass on the pipelined kernel (a single block) or on k_cam
     // together with the epilogue (all blocks, the RHS), the epilogue alone (U^-1, x, v,
@@ -924,33 +943,81 @@ static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term
     if (c_hi == c_lo + 1) {
       launch_cam<S, true, EP_NONE, false>(
           c, cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
-      launch_cam<S, false, EP, false>(c, cam_args(0, 0, 0, 0, 0, term, thr, check_stop));
+      launch_cam<S, false, EP, false>(c, ep_args(cam_args(0, 0, 0, 0, 0, term, thr, check_stop)));
     } else {
-      launch_cam<S, true, EP, false>(c,
-                                     cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
+      launch_cam<S, true, EP, false>(c, ep_args(cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop)));
     }
     launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, 1));
   } else if (!c->collective()) {
-    launch_cam<S, true, EP, true>(c, cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop));
+    launch_cam<S, true, EP, true>(c, ep_args(cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop)));
   } else {
     launch_cam<S, true, EP_NONE, false>(c,
                                         cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop));
     c->allreduce(c->cy, (size_t)c->n_p * 12);
-    launch_cam<S, false, EP, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, check_stop));
+    launch_cam<S, false, EP, true>(c, ep_args(cam_args(0, 0, 0, 0, 1, term, thr, check_stop)));
   }
 }
 
 // one power-series term i >= 1 (s of block 0 already scattered by the previous kernel)
 template <int S>
-static void launch_term(pv_ctx* c, int i, double thr) {
+static void launch_term(pv_ctx* c, int i, double thr, unsigned long long cond = 0,
+                        int max_order = 0) {
   const int B = c->n_blk;
   for (int b = 0; b < B; ++b) {
     launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
     if (b + 1 < B)
       launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, i, thr, 1));
     else
-      launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, i, thr, 1);
+      launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, i, thr, 1, cond, max_order);
   }
+}
+
+// The term loop as ONE CUDA graph: a WHILE conditional node whose body is one term (its
+// kernels captured once, the term index read from the control block); the epilogue kernel
+// of each term sets the condition (continue while not stopped and term < max_order), so the
+// whole series runs with no host round trip per term (solvers.py:140-149).  Cached per
+// configuration; single-process contexts only (the loopback group synchronizes on the
+// host between ranks, which a graph cannot).
+template <int S>
+static TermGraph& term_graph(pv_ctx* c, int max_order, double thr) {
+  TermGraph& G = c->tgraph;
+  const int xm = c->xm_ok ? 1 : 0;
+  if (G.exec && G.stage == S && G.max_order == max_order && G.thr == thr && G.n_blk == c->n_blk &&
+      G.wpc == c->wpc && G.xm == xm && G.coll == c->collective() &&
+      std::memcmp(&G.tune, &c->tune, sizeof(Tune)) == 0)
+    return G;
+  if (G.exec) cudaGraphExecDestroy(G.exec);
+  if (G.graph) cudaGraphDestroy(G.graph);
+  G = TermGraph{};
+  CK(cudaGraphCreate(&G.graph, 0));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, G.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = handle;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, G.graph, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  const long long l0 = c->launches;
+  CK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeRelaxed));
+  launch_term<S>(c, -1, thr, (unsigned long long)handle, max_order);
+  cudaGraph_t captured = nullptr;
+  CK(cudaStreamEndCapture(c->stream, &captured));
+  G.body_launches = c->launches - l0;
+  c->launches = l0;  // counted per executed term instead (op_power)
+  CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+  G.stage = S;
+  G.max_order = max_order;
+  G.thr = thr;
+  G.n_blk = c->n_blk;
+  G.wpc = c->wpc;
+  G.xm = xm;
+  G.tune = c->tune;
+  G.coll = c->collective();
+  return G;
 }
 
 template <int S>
@@ -984,6 +1051,7 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   CK(cudaMemsetAsync(c->flags + F_ZERO_NORM, 0, sizeof(int), c->stream));
   c->sync();
   std::memset(c->host_ctl, 0, sizeof(PowerCtl));
+  CK(cudaEventRecord(c->tev[0], c->stream));
   // K4: t = V+ b_l for all landmarks, then y = W t over all blocks, the reduced RHS,
   // t_0 = U^-1 rhs and the gather of block 0 (a single pass; blocking does not pay here)
   const int B = c->n_blk;
@@ -1000,6 +1068,29 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     mark_rhs<S>(c);
   }
   c->check_launch();
+  CK(cudaEventRecord(c->tev[1], c->stream));
+  int launched_terms = 0;
+  if (c->tune.graph && !c->loop && max_order > 0) {  // the device-driven term loop
+    TermGraph& G = term_graph<S>(c, max_order, thr);
+    CK(cudaGraphLaunch(G.exec, c->stream));
+    CK(cudaEventRecord(c->tev[2], c->stream));
+    back_substitute_dev<S>(c);
+    CK(cudaEventRecord(c->tev[3], c->stream));
+    PowerCtl h;
+    CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    c->launches += G.body_launches * h.term;  // kernels of the executed terms
+    *order = h.order;
+    *trunc = h.trunc;
+    c->step_stage = S;
+    for (int q = 0; q < 3; ++q) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->tev[q], c->tev[q + 1]));
+      c->solve_us[q] = (int64_t)(1000.0 * ms);
+    }
+    c->solve_terms_launched = h.term;
+    return;
+  }
   // K5 + K6 terms with a one-term lookahead on the device stop flag.  The decision to stop
   // launching must be the same on every rank (each launch of a term holds collectives):
   // after term i-1 is known complete, stop only on a stop taken AT a term <= i-1 -- a faster
@@ -1007,6 +1098,7 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   // than the others (the loopback test caught exactly that divergence).
   for (int i = 1; i <= max_order; ++i) {
     launch_term<S>(c, i, thr);
+    ++launched_terms;
     CK(cudaEventRecord(c->ev[i & 1], c->stream));
     if (i >= 2) {
       CK(cudaEventSynchronize(c->ev[(i - 1) & 1]));
@@ -1015,13 +1107,21 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     }
   }
   c->check_launch();
+  CK(cudaEventRecord(c->tev[2], c->stream));
   back_substitute_dev<S>(c);
+  CK(cudaEventRecord(c->tev[3], c->stream));
   PowerCtl h;
   CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   *order = h.order;
   *trunc = h.trunc;
   c->step_stage = S;
+  for (int q = 0; q < 3; ++q) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->tev[q], c->tev[q + 1]));
+    c->solve_us[q] = (int64_t)(1000.0 * ms);
+  }
+  c->solve_terms_launched = launched_terms;
 }
 
 // K5 as apply_schur inside block-Jacobi PCG (solvers.py:153-187)
@@ -1311,6 +1411,8 @@ void pv_destroy(pv_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto e : c->bev)
     if (e) cudaEventDestroy(e);
+  if (c->tgraph.exec) cudaGraphExecDestroy(c->tgraph.exec);
+  if (c->tgraph.graph) cudaGraphDestroy(c->tgraph.graph);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1337,6 +1439,11 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_BLOCKS] = c->n_blk;
   out[PV_INFO_PERSIST_L2] = c->persist_l2;
   out[PV_INFO_WARPS_PER_CAM] = c->wpc;
+  out[PV_INFO_SOLVE_RHS_US] = c->solve_us[0];
+  out[PV_INFO_SOLVE_TERMS_US] = c->solve_us[1];
+  out[PV_INFO_SOLVE_BACKSUB_US] = c->solve_us[2];
+  out[PV_INFO_SOLVE_TERMS_LAUNCHED] = c->solve_terms_launched;
+  out[PV_INFO_XM_BYTES] = (c->xm_ok && c->tune.xm && c->tune.cam_pipe && c->wpc == 1) ? 40 : 48;
   API_END(c)
 }
 
@@ -1375,6 +1482,9 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_RHS_REUSE:
       c->tune.rhs_reuse = value ? 1 : 0;
+      break;
+    case PV_OPT_GRAPH:
+      c->tune.graph = value ? 1 : 0;
       break;
     case PV_OPT_XM:
       c->tune.xm = value ? 1 : 0;

@@ -40,6 +40,7 @@ struct Tune {
   int split_last;    // a term's last block: pipelined W t, then epilogue + next W^T v
   int rhs_reuse;     // reuse the reduced RHS across solves of one POSE_ONLY linearization
   int cost_cs;       // cost over the camera-sorted segments (k_cost_cs) instead of k_cost
+  int graph;         // power-series term loop as a CUDA graph WHILE node (no host round trips)
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -219,6 +220,11 @@ struct CamArgs {
   int wpc;          // warps per camera (1, 2, 4, 8)
   int disc_lo, disc_hi;  // landmark-sorted observations whose consumed partials s are dropped
   double thr;
+  // device-driven term loop (povar.cu term_graph): term < 0 takes the term index from the
+  // control block (previous term + 1); cond != 0 is the WHILE handle of the CUDA graph the
+  // epilogue sets to continue (not stopped and term < max_order) or stop
+  unsigned long long cond;
+  int max_order;
 };
 
 #ifndef PV_CAM_MINB
@@ -491,15 +497,19 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       c.term = 0;
       c.trunc = XN > 0.0 ? 1.0 : 0.0;
     } else {  // solvers.py:140-149
+      const int term = ca.term >= 0 ? ca.term : c.term + 1;
       const double ratio = XN > 0.0 ? TN / XN : 0.0;
       c.trunc = ratio;
-      c.term = ca.term;
+      c.term = term;
       if (ratio <= ca.thr) {
-        c.order = ca.term - 1;
+        c.order = term - 1;
         c.stopped = 1;
       } else {
-        c.order = ca.term;
+        c.order = term;
       }
+      if (ca.cond)
+        cudaGraphSetConditional((cudaGraphConditionalHandle)ca.cond,
+                                (!c.stopped && term < ca.max_order) ? 1u : 0u);
     }
     c.xnorm = XN;
     c.tnorm = TN;

@@ -38,7 +38,8 @@ def test_pipe_matches_k_cam(pv, stage):
         pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"])
     outs = []
     variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_XM, 0)])
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_XM, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_GRAPH, 0)])
     for knobs in variants:
         dp = _ctx(pv, z, knobs)
         info = dp.info()
@@ -237,3 +238,29 @@ def test_cost_camera_sorted_degenerate_depth(pv):
     dp.set_option(_lib.PV_OPT_COST_CS, 1)
     dp.set_state(st)
     assert dp.cost(2) == np.inf
+
+
+@pytest.mark.parametrize("max_order,thr", [(20, 0.01), (20, 0.0), (3, 0.0), (1, 0.01)])
+def test_graph_term_loop_matches_host_loop(pv, max_order, thr):
+    """PV_OPT_GRAPH: the term loop as a CUDA graph WHILE node (device-side stop test) gives
+    the host loop's order, truncation and steps bit for bit -- stop by threshold, by the order
+    cap, and a one-term series; and the captured graph is reused across solves."""
+    from paper_2405_05079_b200 import _lib
+    z = golden("tiny_lm.npz")
+    st = pv.ProjectiveState(z["cams"], z["lms"])
+    outs = []
+    for graph in (0, 1):
+        dp = _ctx(pv, z, [(_lib.PV_OPT_GRAPH, graph)])
+        sysm = pv.assemble_system(dp.problem, st, 1, 1e-4, "pose_only", dp=dp)
+        cfg = pv.SolverConfig(max_power_order=max_order, power_threshold=thr)
+        reps = [pv.power_schur_solve(sysm, cfg) for _ in range(2)]
+        assert reps[0].power_order_used == reps[1].power_order_used
+        np.testing.assert_array_equal(reps[0].pose_update, reps[1].pose_update)
+        outs.append(reps[0])
+    a, b = outs
+    assert a.power_order_used == b.power_order_used
+    assert a.truncation_estimate == b.truncation_estimate
+    np.testing.assert_array_equal(a.pose_update, b.pose_update)
+    np.testing.assert_array_equal(a.landmark_update, b.landmark_update)
+    if thr == 0.0:
+        assert a.power_order_used == max_order
