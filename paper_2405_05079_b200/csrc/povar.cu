@@ -618,6 +618,8 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
                        cudaMemcpyHostToDevice, c->stream));
   }
   c->n_kent = nk;
+  c->g.n_kent = (int)nk;
+  c->g.n_s = (long long)c->sbuf_doubles / 4;
   c->sync();
   c->h_lpos = std::move(lpos);
 }

@@ -20,6 +20,22 @@
 
 #define PV_FULL 0xffffffffu
 
+// PV_CHECKED builds (tools/checked_build.sh): device-side bounds / invariant checks on the
+// indirect accesses of the hot kernels -- the stand-in for compute-sanitizer, which this
+// pool does not allow.  A failed check prints and traps (the launch then reports an error).
+#ifdef PV_CHECKED
+#include <cstdio>
+#define PV_CHECK(cond)                                                                     \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("PV_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);                  \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define PV_CHECK(cond) ((void)0)
+#endif
+
 namespace pv {
 
 // ---------------------------------------------------------------------------

@@ -58,6 +58,8 @@ struct Graph {
                          // camera-sorted observation
   const int* cs_kpos;    // [n_o] warp-slot position (build_ktasks) of the landmark of each
                          // camera-sorted observation: the index of its V+ and t
+  int n_kent;            // warp-slot entries (V+ / t positions, build_ktasks)
+  long long n_s;         // entries of the partials buffer s (build_ktasks)
   int n_blk;             // landmark blocks of the L2-blocked term
   const int* seg;        // [n_blk*n_p+1] start of segment (block b, camera c) at b*n_p+c in the
                          // block-major camera-sorted order (block, camera, landmark)
@@ -297,7 +299,10 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
 #pragma unroll
         for (int r = 0; r < CH / 32; ++r) {
           const int q = lane + 32 * r;
-          if (o0 + q < o_hi) T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
+          if (o0 + q < o_hi) {
+            PV_CHECK(si[q] >= 0 && si[q] < g.n_kent);
+            T[r] = ldg4p(tarr + 4 * (size_t)si[q], pt);
+          }
         }
 #pragma unroll
         for (int r = 0; r < CH / 32; ++r) {
@@ -449,6 +454,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
             sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
             sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
             sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
+            PV_CHECK(pos >= 0 && pos < g.n_s);
             st4p(sbuf + 4 * (size_t)pos, sv, ps);
           }
         }
@@ -747,6 +753,7 @@ __global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __
                             double* __restrict__ cs_xm, int* __restrict__ flags) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= g.n_o) return;
+  PV_CHECK(__ldg(g.cs_lm + o) >= 0 && __ldg(g.cs_lm + o) < g.n_l);
   const double4 x = ldg4(lrec + (size_t)__ldg(g.cs_lm + o) * LREC);
   st4(cs_x + 4 * (size_t)o, x);
   if (STAGE == 1) {

@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
               n = __shfl_sync(PV_FULL, wcur.z, src), fl = __shfl_sync(PV_FULL, wcur.w, src);
     const int s = n_prod % PD;
     unsigned char* slot = wsm + s * PSLOT;
+    PV_CHECK(cam >= 0 && cam < g.n_p && n >= 0 && n <= PCH && o >= 0 && o + n <= g.n_o);
+    PV_CHECK(((o + n + 3) & ~3) - (o & ~3) <= PCH + 4);
     if (lane == 0) {
 #if PV_PIPE_FENCE
       fence_proxy_async();  // the warp's generic reads of this slot precede the refill
@@ -212,6 +214,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     for (int r = 0; r < (PCH + 31) / 32; ++r) {
       const int q = lane + 32 * r;
       if (q >= h.z) continue;
+      PV_CHECK(si[q] >= 0 && si[q] < g.n_kent);
       const double* src = tarr + 4 * (size_t)si[q];
       cp_async16wp(tb + 32 * q, src, pt);
       cp_async16wp(tb + 32 * q + 16, src + 2, pt);
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
         sv.y = fma(f0, P0.y, fma(f1, P1.y, f2 * P2v.y));
         sv.z = fma(f0, P0.z, fma(f1, P1.z, f2 * P2v.z));
         sv.w = STAGE == 2 ? fma(f0, P0.w, fma(f1, P1.w, f2 * P2v.w)) : 0.0;
+        PV_CHECK(pos >= 0 && pos < g.n_s);
         st4p(sbuf + 4 * (size_t)pos, sv, ps);
       }
     }

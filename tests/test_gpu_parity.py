@@ -3,9 +3,10 @@
 Tolerances follow BASELINE.json's north_star: per-kernel outputs within 1e-10
 relative (norm-wise over the whole output), LM cost traces
 within 1e-6 relative over the first 20 iterations with the same accept/reject
-sequence.  Stage-2 reduced RHS entries are cancellation-limited, so they are
-compared relative to ||b_p|| (the oracle itself differs from the reference by
-~1e-10 there).
+sequence.  The one exception is the stage-2 reduced RHS, a cancellation: the CPU
+oracle itself differs from the reference by 9.1e-11 there, so it is bounded at
+3e-10 relative and 1e-12 of ||b_p||, with the trial cost that inherits it at 1e-9.
+Every check() logs its achieved error (PV_PARITY_REPORT).
 """
 
 import math
@@ -82,7 +83,8 @@ def test_stage1_blocks_and_power(pv, mini, tag, both):
         cfg = pv.SolverConfig(max_power_order=20, power_threshold=thr)
         rep = pv.power_schur_solve(sysm, cfg)
         assert rep.power_order_used == int(z[tag + f"pow_{t2}_order"])
-        assert abs(rep.truncation_estimate - float(z[tag + f"pow_{t2}_trunc"])) <= 1e-9
+        check(tag + f"trunc({t2})", abs(rep.truncation_estimate - float(z[tag + f"pow_{t2}_trunc"])),
+              1e-10)
         check(tag + f"dx({t2})", rel(rep.pose_update, z[tag + f"pow_{t2}_dx"]), TOL)
         check(tag + f"dl({t2})", rel(rep.landmark_update, z[tag + f"pow_{t2}_dl"]), TOL)
     check(tag + "rhs", rel(dp.debug(_lib.PV_DBG_RHS)[:, :12].ravel(), z[tag + "rhs"]), TOL)
@@ -106,15 +108,20 @@ def test_stage2_blocks_and_power(pv, mini):
     cfg = pv.SolverConfig(max_power_order=20, power_threshold=0.01)
     rep = pv.power_schur_solve(sysm, cfg)
     rhs = dp.debug(_lib.PV_DBG_RHS)[:, :11].ravel()
-    check("s2_rhs/|b_p|", np.linalg.norm(rhs - z["s2_rhs"]) / np.linalg.norm(z["s2_b_p"]), 1e-9)
-    check("s2_rhs", rel(rhs, z["s2_rhs"]), 1e-6)
+    # the stage-2 reduced RHS -(b_p - W V+ b_l) cancels: the CPU oracle (NumPy, the
+    # reference's own libraries, another summation order) differs from the reference by
+    # 9.1e-11 relative here (1.4e-13 of |b_p|), so 1e-10 is below the floor of any other
+    # summation order; the bound is 3e-10 (the achieved error is logged)
+    check("s2_rhs/|b_p|", np.linalg.norm(rhs - z["s2_rhs"]) / np.linalg.norm(z["s2_b_p"]), 1e-12)
+    check("s2_rhs", rel(rhs, z["s2_rhs"]), 3e-10)
     assert rep.power_order_used == int(z["s2_pow_thr_order"])
-    check("s2_dx", rel(rep.pose_update, z["s2_pow_thr_dx"]), 1e-8)
+    check("s2_dx", rel(rep.pose_update, z["s2_pow_thr_dx"]), 1e-10)
     # trial state through the device retraction
     assert dp.trial(2)
     trial = dp.get_state(trial=True)
-    check("s2_trial_cams", rel(trial.cameras, z["s2_trial_cams"]), 1e-8)
-    check("s2_trial_cost", rel(dp.cost(2, trial=True), z["s2_trial_cost"]), 1e-8)
+    check("s2_trial_cams", rel(trial.cameras, z["s2_trial_cams"]), 1e-10)
+    # the projective trial cost amplifies the step's (RHS-cancellation) error
+    check("s2_trial_cost", rel(dp.cost(2, trial=True), z["s2_trial_cost"]), 1e-9)
 
 
 @pytest.mark.parametrize("tag,stage,kw", [
@@ -162,7 +169,7 @@ def test_tiny_stage2_trace(pv):
     st = _state(pv, z, "s2_cams0", "s2_lms0")
     rep = pv.riemannian_step(dp.problem, st, pv.SolverConfig(max_outer_iterations=20), dp=dp)
     assert rep.power_order_used == int(z["s2_it1_order"])
-    assert rel(rep.pose_update, z["s2_it1_dx"]) <= 1e-8
+    check("tiny s2 it1 dx", rel(rep.pose_update, z["s2_it1_dx"]), 1e-10)
     final, trace = pv.lm_minimize(dp.problem, st, 2, pv.SolverConfig(max_outer_iterations=20),
                                   dp=dp)
     costs = np.array([r.cost for r in trace.records])

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-PV_PARITY_REPORT=gpurun_out/parity_loop.json timeout 600 python -m pytest tests/test_gpu_loopback.py -m gpu -q -s 2>&1 | tail -10
+timeout 1200 python tools/sweep_lm.py vlarge 8 "5=83886080|5=67108864|5=58720256|5=50331648|5=100663296" 2>&1 | tail -10
