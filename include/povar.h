@@ -105,9 +105,15 @@ enum {
   PV_OPT_XM = 14,              /* 1 (default): stage-1 pipelined camera passes stream x and m as
                                   (x0 x1 x2 m0 | m1), 40 instead of 48 bytes per observation,
                                   when every landmark has w = 1                             */
-  PV_OPT_GRAPH = 15            /* 1 (default): the power-series term loop runs as one CUDA graph
+  PV_OPT_GRAPH = 15,           /* 1 (default): the power-series term loop runs as one CUDA graph
                                   (WHILE conditional node, stop test on the device); 0: host
                                   loop with a one-term look-ahead                            */
+  PV_OPT_BALANCE = 16,         /* work lists of the persistent camera kernel: 1 (default) whole
+                                  cameras packed longest-first (W t) and item-granular cuts
+                                  (W^T v); 0 contiguous equal-cost camera ranges              */
+  PV_OPT_BAL_ITEM = 17,        /* cost model of that balance, in observation-equivalents: fixed */
+  PV_OPT_BAL_ROUND = 18,       /* cost of an item, of each 32-observation round, and of a        */
+  PV_OPT_BAL_LAST = 19         /* camera's last W t item (its warp reduction)                    */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

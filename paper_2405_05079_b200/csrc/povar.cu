@@ -12,6 +12,9 @@
 #include <cmath>
 #include <condition_variable>
 #include <mutex>
+#include <numeric>
+#include <queue>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -102,7 +105,7 @@ __global__ void k_loop_max(int world, const int* const* bufs, int n, int* out) {
 
 // a captured term loop (term_graph) and the configuration it was captured for
 struct TermGraph {
-  int stage = 0, max_order = 0, n_blk = 0, wpc = 0, xm = 0;
+  int stage = 0, max_order = 0, n_blk = 0, wpc = 0, xm = 0, layout_gen = -1;
   double thr = 0.0;
   Tune tune{};
   bool coll = false;
@@ -165,6 +168,10 @@ struct pv_ctx {
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
+  std::vector<int> h_seg;  // [(n_blk * n_p) + 1] (block, camera) segment starts (re-balancing)
+  // cost model of the work-list balance, in observation-equivalents (PV_OPT_BALANCE ...)
+  int bal_mode = 1, bal_item = 24, bal_round = 0, bal_last = 0;
+  int layout_gen = 0;  // bumped whenever device work lists are rebuilt (term-graph cache key)
   int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
 
@@ -432,10 +439,19 @@ static void ensure_cpart(pv_ctx* c) {
   c->cpart_cap = need;
 }
 
-// Work lists of k_cam_pipe (pv_pipe.cuh): for every landmark block and both passes,
-// split the cameras into pipe_W contiguous ranges of equal cost (observations + a
-// per-item overhead) and cut each (camera, block) segment into items of <= PCH
-// observations.  The W t list has >= 1 item per camera so that y is always written.
+// Work lists of k_cam_pipe (pv_pipe.cuh).  Every (camera, block) segment is cut into items of
+// <= PCH observations; per landmark block there are three families of per-warp lists:
+//   0: W t items (>= 1 per camera so that y is always written).  A camera's items stay with
+//      one warp (it owns the camera's sum);
+//   1: W^T v items for a pass launched on its own;
+//   2: W^T v items of block b for the launch that also runs the W t items of block b - 1.
+// Balance (bal_mode 1): the cost of an item is n + bal_item + bal_round * ceil(n / 32)
+// (+ bal_last on a camera's last W t item), in observation-equivalents.  Family 0 packs
+// whole cameras longest-first onto the least loaded warp; W^T v items are independent, so
+// families 1 and 2 cut the stream at item granularity, family 2 giving each warp what its
+// W t list of block b - 1 leaves below the launch's mean.  With contiguous equal-cost camera
+// ranges (bal_mode 0, round 1) the heaviest warp carried 17-18% more than the mean at vlarge
+// (a camera's segment is ~1/6 of a warp's share) and the launch waited for it.
 static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
   if (!c->pipe_W) {
     int occ = 1 << 30;
@@ -458,38 +474,129 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
   }
   const int B = c->n_blk, W = c->pipe_W;
   const int64_t np = c->n_p;
-  constexpr int ITEM_COST = 24;  // observation-equivalents of one item's fixed overhead
+  const int IC = c->bal_item, RC = c->bal_round, LC = c->bal_last;
+  auto item_cost = [&](int n, bool last_hc) {
+    return (int64_t)n + IC + (int64_t)RC * ((n + 31) / 32) + (last_hc ? LC : 0);
+  };
   std::vector<int4> items;
-  std::vector<int> off((size_t)2 * B * (W + 1), 0);
-  items.reserve((size_t)2 * ((size_t)c->n_os / PCH + (size_t)B * np + 16));
-  for (int L = 0; L < 2; ++L) {
+  std::vector<int> off((size_t)3 * B * (W + 1), 0);
+  items.reserve((size_t)3 * ((size_t)c->n_os / PCH + (size_t)B * np + 16));
+  auto push_cam = [&](int64_t cam, const int* sb, int L) {  // all items of one camera
+    const int o_lo = sb[cam], n = sb[cam + 1] - o_lo;
+    const int k0 = (n + PCH - 1) / PCH, k = L == 0 ? std::max(1, k0) : k0;
+    for (int q = 0; q < k; ++q) {
+      const int o = o_lo + q * PCH;
+      const int cnt = std::max(0, std::min(PCH, o_lo + n - o));
+      items.push_back(make_int4((int)cam, o, cnt, (L ? PF_HA : 0) | (q == k - 1 ? PF_LAST : 0)));
+    }
+  };
+  auto cam_cost = [&](int64_t cam, const int* sb, int L) {
+    const int n = sb[cam + 1] - sb[cam];
+    const int k0 = (n + PCH - 1) / PCH, k = L == 0 ? std::max(1, k0) : k0;
+    int64_t t = 0;
+    for (int q = 0; q < k; ++q)
+      t += item_cost(std::max(0, std::min(PCH, n - q * PCH)), L == 0 && q == k - 1);
+    return t;
+  };
+  std::vector<std::vector<int64_t>> hc_load(B, std::vector<int64_t>(W, 0));
+  double worst[3] = {1.0, 1.0, 1.0};
+  for (int L = 0; L < 3; ++L) {
     for (int b = 0; b < B; ++b) {
       const int* sb = seg.data() + (size_t)b * np;
-      auto n_items = [&](int64_t cam) {
-        const int n = sb[cam + 1] - sb[cam];
-        const int k = (n + PCH - 1) / PCH;
-        return L == 0 ? std::max(1, k) : k;
-      };
-      int64_t tot = 0;
-      for (int64_t cam = 0; cam < np; ++cam) tot += (sb[cam + 1] - sb[cam]) + ITEM_COST * n_items(cam);
       int* ob = off.data() + (size_t)(L * B + b) * (W + 1);
       ob[0] = (int)items.size();
-      int64_t cum = 0;
-      int w = 0;
-      for (int64_t cam = 0; cam < np; ++cam) {
-        // contiguous camera ranges: start the next warp once its cost share is reached
-        while (w < W - 1 && cum * W >= (int64_t)(w + 1) * tot) ob[++w] = (int)items.size();
-        const int o_lo = sb[cam], n = sb[cam + 1] - o_lo, k = n_items(cam);
-        for (int q = 0; q < k; ++q) {
-          const int o = o_lo + q * PCH;
-          const int cnt = std::max(0, std::min(PCH, o_lo + n - o));
-          items.push_back(make_int4((int)cam, o, cnt, (L ? PF_HA : 0) | (q == k - 1 ? PF_LAST : 0)));
+      if (c->bal_mode == 0) {  // contiguous camera ranges of equal cost
+        int64_t tot = 0, cum = 0;
+        for (int64_t cam = 0; cam < np; ++cam) tot += cam_cost(cam, sb, L);
+        int w = 0;
+        for (int64_t cam = 0; cam < np; ++cam) {
+          while (w < W - 1 && cum * W >= (int64_t)(w + 1) * tot) ob[++w] = (int)items.size();
+          push_cam(cam, sb, L);
+          cum += cam_cost(cam, sb, L);
         }
-        cum += n + ITEM_COST * k;
+        while (w < W) ob[++w] = (int)items.size();
+        continue;
       }
-      while (w < W) ob[++w] = (int)items.size();
+      if (L == 0) {  // whole cameras, longest first onto the least loaded warp
+        std::vector<std::pair<int64_t, int>> cams((size_t)np);
+        for (int64_t cam = 0; cam < np; ++cam) cams[cam] = {cam_cost(cam, sb, 0), (int)cam};
+        std::stable_sort(cams.begin(), cams.end(),
+                         [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& x) {
+                           return a.first > x.first;
+                         });
+        using Slot = std::pair<int64_t, int>;  // (load, warp): smallest load first, then warp
+        std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+        for (int w = 0; w < W; ++w) heap.push({0, w});
+        std::vector<std::vector<int>> mine(W);
+        for (const auto& cc : cams) {
+          Slot s = heap.top();
+          heap.pop();
+          mine[s.second].push_back(cc.second);
+          s.first += cc.first;
+          heap.push(s);
+        }
+        int64_t tot = 0, mx = 0;
+        for (int w = 0; w < W; ++w) {
+          std::sort(mine[w].begin(), mine[w].end());
+          int64_t load = 0;
+          for (int cam : mine[w]) {
+            push_cam(cam, sb, 0);
+            load += cam_cost(cam, sb, 0);
+          }
+          hc_load[b][w] = load;
+          tot += load;
+          mx = std::max(mx, load);
+          ob[w + 1] = (int)items.size();
+        }
+        if (tot > 0) worst[0] = std::max(worst[0], (double)mx * W / (double)tot);
+        continue;
+      }
+      // W^T v: cut the item stream so that warp w ends at its share of the cumulative cost
+      const size_t first = items.size();
+      int64_t tot_a = 0;
+      for (int64_t cam = 0; cam < np; ++cam) {
+        push_cam(cam, sb, 1);
+        tot_a += cam_cost(cam, sb, 1);
+      }
+      std::vector<double> want(W, 1.0);
+      if (L == 2 && b > 0) {
+        int64_t tot_c = 0;
+        for (int w = 0; w < W; ++w) tot_c += hc_load[b - 1][w];
+        const double mean = (double)(tot_c + tot_a) / W;
+        for (int w = 0; w < W; ++w) want[w] = std::max(0.0, mean - (double)hc_load[b - 1][w]);
+      }
+      double wsum = 0.0;
+      for (int w = 0; w < W; ++w) wsum += want[w];
+      if (wsum <= 0.0) {
+        std::fill(want.begin(), want.end(), 1.0);
+        wsum = W;
+      }
+      size_t i = first;
+      double cum = 0.0, bound = 0.0, mx = 0.0;
+      for (int w = 0; w < W; ++w) {
+        bound += want[w] / wsum * (double)tot_a;
+        const double start = cum;
+        while (i < items.size()) {  // an item goes to the warp that holds its midpoint
+          const double ci = (double)item_cost(items[i].z, false);
+          if (w < W - 1 && cum + 0.5 * ci > bound) break;
+          cum += ci;
+          ++i;
+        }
+        ob[w + 1] = (int)i;
+        mx = std::max(mx, cum - start + (L == 2 && b > 0 ? (double)hc_load[b - 1][w] : 0.0));
+      }
+      const double mean_l =
+          L == 2 && b > 0
+              ? ((double)tot_a + (double)std::accumulate(hc_load[b - 1].begin(), hc_load[b - 1].end(),
+                                                         (int64_t)0)) / W
+              : (double)tot_a / W;
+      if (mean_l > 0) worst[L] = std::max(worst[L], mx / mean_l);
     }
   }
+  if (std::getenv("PV_DEBUG_BALANCE"))
+    std::fprintf(stderr, "pipe items: B=%d W=%d mode=%d cost(item=%d round=%d last=%d) worst max/mean: "
+                 "Wt %.4f  WTv %.4f  paired %.4f\n", B, W, c->bal_mode, IC, RC, LC, worst[0], worst[1],
+                 worst[2]);
   free_tracked(c, c->d_items, c->items_bytes);
   free_tracked(c, c->d_item_off, c->item_off_bytes);
   c->d_items = c->alloc<int4>(items.size());
@@ -501,6 +608,7 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
   CK(cudaMemcpyAsync(c->d_item_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice,
                      c->stream));
   c->sync();
+  ++c->layout_gen;
 }
 
 // Work of the landmark reduce (k_lm_reduce, pv_kernels.cuh) and of the lane-per-landmark
@@ -692,6 +800,7 @@ static void build_blocks(pv_ctx* c) {
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
   build_pipe_items(c, seg);
+  c->h_seg = seg;
   build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
   if (c->cpart) ensure_cpart(c);   // re-blocking changes the number of warp slots
 }
@@ -891,7 +1000,8 @@ static void launch_cam(pv_ctx* c, const CamArgs& ca0) {
   // the persistent kernel runs one warp per camera: with wpc == 1 it reproduces k_cam's
   // summation order bit for bit, so every path (fused, sharded, blocked) stays consistent
   if (EP == EP_NONE && c->tune.cam_pipe && c->wpc == 1 && !ca.project_y &&
-      (!HC || ca.c_hi == ca.c_lo + 1) && (!HA || ca.a_hi == ca.a_lo + 1)) {
+      (!HC || ca.c_hi == ca.c_lo + 1) && (!HA || ca.a_hi == ca.a_lo + 1) &&
+      (!(HC && HA) || ca.a_lo == ca.c_lo + 1)) {  // the paired W^T v lists assume block b + 1
     launch_cam_pipe<S, HC, HA>(c, ca);
     return;
   }
@@ -986,6 +1096,7 @@ static TermGraph& term_graph(pv_ctx* c, int max_order, double thr) {
   const int xm = c->xm_ok ? 1 : 0;
   if (G.exec && G.stage == S && G.max_order == max_order && G.thr == thr && G.n_blk == c->n_blk &&
       G.wpc == c->wpc && G.xm == xm && G.coll == c->collective() &&
+      G.layout_gen == c->layout_gen &&
       std::memcmp(&G.tune, &c->tune, sizeof(Tune)) == 0)
     return G;
   if (G.exec) cudaGraphExecDestroy(G.exec);
@@ -1017,6 +1128,7 @@ static TermGraph& term_graph(pv_ctx* c, int max_order, double thr) {
   G.n_blk = c->n_blk;
   G.wpc = c->wpc;
   G.xm = xm;
+  G.layout_gen = c->layout_gen;
   G.tune = c->tune;
   G.coll = c->collective();
   return G;
@@ -1503,6 +1615,15 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_CAM_PIPE:
       c->tune.cam_pipe = value ? 1 : 0;
       break;
+    case PV_OPT_BALANCE:
+    case PV_OPT_BAL_ITEM:
+    case PV_OPT_BAL_ROUND:
+    case PV_OPT_BAL_LAST:
+      if (value < 0 || value > 4096) throw PvError(PV_EINVAL, "balance option out of range");
+      (key == PV_OPT_BALANCE ? c->bal_mode : key == PV_OPT_BAL_ITEM ? c->bal_item
+       : key == PV_OPT_BAL_ROUND ? c->bal_round : c->bal_last) = (int)value;
+      build_pipe_items(c, c->h_seg);
+      break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
       c->block_bytes = value;
@@ -1833,6 +1954,24 @@ int pv_bench_terms(pv_ctx* c, int stage, int n, float* ms) {
   API_END(c)
 }
 
+
+#ifdef PV_PIPE_TIMING
+// diagnostic build only (not part of include/povar.h): per-warp timers of the fused camera
+// launch of block `block` in whatever ran last, and the work lists they belong to
+int pv_debug_pipe_times(pv_ctx* c, int block, unsigned long long* t /*3*W*/, int* n_items,
+                        int4* items /*cap*/, int cap, int* off /*3*B*(W+1)*/) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  c->sync();
+  if (t) CK(cudaMemcpyFromSymbol(t, g_pipe_t, sizeof(unsigned long long) * 3 * std::min(c->pipe_W, 8192)));
+  CK(cudaMemcpyToSymbol(g_pipe_dbg_block, &block, sizeof(int)));
+  const int n = (int)(c->items_bytes / sizeof(int4));
+  if (n_items) *n_items = n;
+  if (items) CK(cudaMemcpy(items, c->d_items, sizeof(int4) * std::min(n, cap), cudaMemcpyDeviceToHost));
+  if (off) CK(cudaMemcpy(off, c->d_item_off, c->item_off_bytes, cudaMemcpyDeviceToHost));
+  API_END(c)
+}
+#endif
 
 int pv_debug_get(pv_ctx* c, int which, double* out) {
   API_BEGIN(c)

@@ -64,6 +64,18 @@ constexpr int PIPE_SMEM = PBAR + PW * PWARP;
 
 enum { PF_HA = 1, PF_LAST = 2 };
 
+#ifdef PV_PIPE_TIMING
+// diagnostic build (tools/pipe_times.py): per warp of the fused launch of block g_pipe_dbg_block,
+// {globaltimer at entry, after the last W^T v / W t item, SM id}
+__device__ unsigned long long g_pipe_t[3 * 8192];
+__device__ int g_pipe_dbg_block = 5;
+__device__ __forceinline__ unsigned long long pipe_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -107,7 +119,8 @@ __device__ __forceinline__ void fence_proxy_async() {
 // (so y is always written); PF_LAST marks its last one.
 struct PipeItems {
   const int4* item;
-  const int* off;  // [(L * B + b) * (W + 1) + w]: first item of warp w
+  const int* off;  // [(L * B + b) * (W + 1) + w]: first item of warp w; L = 0 W t, 1 W^T v on
+                   // its own, 2 W^T v of block b launched with the W t items of block b - 1
   int B, W;
 };
 
@@ -127,6 +140,9 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
                                                       int check_stop, int disc_lo, int disc_hi) {
   extern __shared__ __align__(128) unsigned char pipe_dsm[];
   if (check_stop && ctl->stopped) return;  // grid-uniform
+#ifdef PV_PIPE_TIMING
+  const unsigned long long t_entry = pipe_gtimer();
+#endif
   discard_s_lines(sbuf, disc_lo, disc_hi);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -146,8 +162,8 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     h0 = __ldg(o);
     nh = __ldg(o + 1) - h0;
   }
-  if (HA) {
-    const int* o = it.off + (size_t)(it.B + ba) * (it.W + 1) + gw;
+  if (HA) {  // family 2 when this launch also runs the W t items of block ba - 1
+    const int* o = it.off + (size_t)((HC ? 2 : 1) * it.B + ba) * (it.W + 1) + gw;
     a0 = __ldg(o);
     na = __ldg(o + 1) - a0;
   }
@@ -323,6 +339,15 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     __syncwarp();
   }
   cp_wait<0>();
+#ifdef PV_PIPE_TIMING
+  if (HC && HA && bc == g_pipe_dbg_block && lane == 0 && gw < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_pipe_t[3 * gw] = t_entry;
+    g_pipe_t[3 * gw + 1] = pipe_gtimer();
+    g_pipe_t[3 * gw + 2] = smid;
+  }
+#endif
 }
 
 }  // namespace pv
