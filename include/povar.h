@@ -113,7 +113,13 @@ enum {
                                   (W^T v); 0 contiguous equal-cost camera ranges              */
   PV_OPT_BAL_ITEM = 17,        /* cost model of that balance, in observation-equivalents: fixed */
   PV_OPT_BAL_ROUND = 18,       /* cost of an item, of each 32-observation round, and of a        */
-  PV_OPT_BAL_LAST = 19         /* camera's last W t item (its warp reduction)                    */
+  PV_OPT_BAL_LAST = 19,        /* camera's last W t item (its warp reduction)                    */
+  PV_OPT_BAL_RFIX = 20,        /* ... and of a landmark-reduce slot of the series kernel: fixed  */
+  PV_OPT_BAL_ROBS8 = 21,       /* + (partials * value) / 8                                       */
+  PV_OPT_SERIES = 22           /* 1 (default): the whole power series (every term's landmark
+                                  reduces, camera passes, U^-1 epilogue and stop test) runs as
+                                  ONE persistent cooperative kernel with grid barriers
+                                  (pv_series.cuh); 0: one launch per landmark block and pass    */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

@@ -19,12 +19,14 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/povar.h"
 #include "pv_kernels.cuh"
 #include "pv_pcg.cuh"
 #include "pv_pipe.cuh"
+#include "pv_series.cuh"
 
 using namespace pv;
 
@@ -171,6 +173,17 @@ struct pv_ctx {
   std::vector<int> h_seg;  // [(n_blk * n_p) + 1] (block, camera) segment starts (re-balancing)
   // cost model of the work-list balance, in observation-equivalents (PV_OPT_BALANCE ...)
   int bal_mode = 1, bal_item = 24, bal_round = 0, bal_last = 0;
+  int bal_rfix = 30, bal_robs8 = 3;  // landmark-reduce slot: fixed + (partials * robs8) / 8
+  // per-warp landmark-reduce slot lists of the series kernel (k_series)
+  int* d_rslot = nullptr;
+  int* d_roff = nullptr;
+  size_t rslot_bytes = 0, roff_bytes = 0;
+  std::vector<int> h_slot_n;  // partials (padding lanes included) of every warp slot
+  unsigned* sbar = nullptr;   // grid barrier of k_series
+  bool skip_next_gather = false;
+  // pinned staging of large pageable host transfers (pv_set_state / pv_get_state)
+  char* stage_pin[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};  // the RHS launches leave block 0's W^T v pass to k_series
   int layout_gen = 0;  // bumped whenever device work lists are rebuilt (term-graph cache key)
   int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
@@ -192,7 +205,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -470,6 +483,9 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
     occ_of((const void*)k_cam_pipe<1, true, true, true>);
     occ_of((const void*)k_cam_pipe<1, false, true, true>);
     occ_of((const void*)k_cam_pipe<1, true, false, true>);
+    occ_of((const void*)k_series<1, false>);
+    occ_of((const void*)k_series<1, true>);
+    occ_of((const void*)k_series<2, false>);
     c->pipe_W = std::max(1, occ) * c->num_sms * PW;
   }
   const int B = c->n_blk, W = c->pipe_W;
@@ -479,8 +495,8 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
     return (int64_t)n + IC + (int64_t)RC * ((n + 31) / 32) + (last_hc ? LC : 0);
   };
   std::vector<int4> items;
-  std::vector<int> off((size_t)3 * B * (W + 1), 0);
-  items.reserve((size_t)3 * ((size_t)c->n_os / PCH + (size_t)B * np + 16));
+  std::vector<int> off((size_t)4 * B * (W + 1), 0);
+  items.reserve((size_t)4 * ((size_t)c->n_os / PCH + (size_t)B * np + 16));
   auto push_cam = [&](int64_t cam, const int* sb, int L) {  // all items of one camera
     const int o_lo = sb[cam], n = sb[cam + 1] - o_lo;
     const int k0 = (n + PCH - 1) / PCH, k = L == 0 ? std::max(1, k0) : k0;
@@ -499,74 +515,131 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
     return t;
   };
   std::vector<std::vector<int64_t>> hc_load(B, std::vector<int64_t>(W, 0));
-  double worst[3] = {1.0, 1.0, 1.0};
-  for (int L = 0; L < 3; ++L) {
+  std::vector<std::vector<int64_t>> r_load(B, std::vector<int64_t>(W, 0));
+  double worst[5] = {1.0, 1.0, 1.0, 1.0, 1.0};
+  using Slot = std::pair<int64_t, int>;  // (load, warp): smallest load first, then warp
+  // longest-first packing of (cost, id) units onto the warps, starting from `init` loads;
+  // mine[w] = the ids of warp w in increasing order, load[w] = its packed cost (init excluded)
+  auto pack = [&](std::vector<std::pair<int64_t, int>>& units, const std::vector<int64_t>* init,
+                  std::vector<std::vector<int>>& mine, std::vector<int64_t>& load) {
+    std::stable_sort(units.begin(), units.end(),
+                     [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& x) {
+                       return a.first > x.first;
+                     });
+    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+    for (int w = 0; w < W; ++w) heap.push({init ? (*init)[w] : 0, w});
+    mine.assign(W, {});
+    load.assign(W, 0);
+    for (const auto& u : units) {
+      Slot sl = heap.top();
+      heap.pop();
+      mine[sl.second].push_back(u.second);
+      sl.first += u.first;
+      load[sl.second] += u.first;
+      heap.push(sl);
+    }
+    for (int w = 0; w < W; ++w) std::sort(mine[w].begin(), mine[w].end());
+  };
+  auto imbalance = [&](const std::vector<int64_t>& a, const std::vector<int64_t>* b2,
+                       const std::vector<int64_t>* b3) {
+    int64_t tot = 0, mx = 0;
+    for (int w = 0; w < W; ++w) {
+      const int64_t v = a[w] + (b2 ? (*b2)[w] : 0) + (b3 ? (*b3)[w] : 0);
+      tot += v;
+      mx = std::max(mx, v);
+    }
+    return tot > 0 ? (double)mx * W / (double)tot : 1.0;
+  };
+  // family 0: W t items, whole cameras per warp
+  for (int b = 0; b < B; ++b) {
+    const int* sb = seg.data() + (size_t)b * np;
+    int* ob = off.data() + (size_t)(0 * B + b) * (W + 1);
+    ob[0] = (int)items.size();
+    if (c->bal_mode == 0) {  // contiguous camera ranges of equal cost
+      int64_t tot = 0, cum = 0;
+      for (int64_t cam = 0; cam < np; ++cam) tot += cam_cost(cam, sb, 0);
+      int w = 0;
+      for (int64_t cam = 0; cam < np; ++cam) {
+        while (w < W - 1 && cum * W >= (int64_t)(w + 1) * tot) ob[++w] = (int)items.size();
+        push_cam(cam, sb, 0);
+        cum += cam_cost(cam, sb, 0);
+        hc_load[b][w] += cam_cost(cam, sb, 0);
+      }
+      while (w < W) ob[++w] = (int)items.size();
+    } else {
+      std::vector<std::pair<int64_t, int>> cams((size_t)np);
+      for (int64_t cam = 0; cam < np; ++cam) cams[cam] = {cam_cost(cam, sb, 0), (int)cam};
+      std::vector<std::vector<int>> mine;
+      pack(cams, nullptr, mine, hc_load[b]);
+      for (int w = 0; w < W; ++w) {
+        for (int cam : mine[w]) push_cam(cam, sb, 0);
+        ob[w + 1] = (int)items.size();
+      }
+    }
+    worst[0] = std::max(worst[0], imbalance(hc_load[b], nullptr, nullptr));
+  }
+  // landmark-reduce slots of block b for k_series, packed on top of the W t load of block
+  // b - 1 (the same step of the series schedule)
+  std::vector<int> rslot;
+  std::vector<int> roff((size_t)B * (W + 1), 0);
+  rslot.reserve(c->h_slot_n.size());
+  for (int b = 0; b < B; ++b) {
+    const int k0 = c->blk_ktask[b], k1 = c->blk_ktask[b + 1];
+    std::vector<std::pair<int64_t, int>> units;
+    units.reserve(k1 - k0);
+    for (int w = k0; w < k1; ++w)
+      units.push_back({(int64_t)c->bal_rfix + ((int64_t)c->h_slot_n[w] * c->bal_robs8) / 8, w});
+    std::vector<std::vector<int>> mine;
+    pack(units, b > 0 ? &hc_load[b - 1] : nullptr, mine, r_load[b]);
+    int* ro = roff.data() + (size_t)b * (W + 1);
+    ro[0] = (int)rslot.size();
+    for (int w = 0; w < W; ++w) {
+      for (int sl : mine[w]) rslot.push_back(sl);
+      ro[w + 1] = (int)rslot.size();
+    }
+    worst[4] = std::max(worst[4], imbalance(r_load[b], b > 0 ? &hc_load[b - 1] : nullptr, nullptr));
+  }
+  // families 1-3: W^T v items of block b, cut at item granularity so that warp w gets what
+  // the other work of its launch / step leaves below the mean: nothing else (1), the W t
+  // items of block b - 1 (2), the reduce slots of block b - 1 and the W t items of block
+  // b - 2 (3, k_series)
+  for (int L = 1; L <= 3; ++L) {
     for (int b = 0; b < B; ++b) {
       const int* sb = seg.data() + (size_t)b * np;
       int* ob = off.data() + (size_t)(L * B + b) * (W + 1);
       ob[0] = (int)items.size();
-      if (c->bal_mode == 0) {  // contiguous camera ranges of equal cost
+      std::vector<int64_t> other(W, 0);
+      if (c->bal_mode != 0) {
+        if (L == 2 && b >= 1) other = hc_load[b - 1];
+        if (L == 3 && b >= 1) {
+          other = r_load[b - 1];
+          if (b >= 2)
+            for (int w = 0; w < W; ++w) other[w] += hc_load[b - 2][w];
+        }
+      }
+      if (c->bal_mode == 0) {
         int64_t tot = 0, cum = 0;
-        for (int64_t cam = 0; cam < np; ++cam) tot += cam_cost(cam, sb, L);
+        for (int64_t cam = 0; cam < np; ++cam) tot += cam_cost(cam, sb, 1);
         int w = 0;
         for (int64_t cam = 0; cam < np; ++cam) {
           while (w < W - 1 && cum * W >= (int64_t)(w + 1) * tot) ob[++w] = (int)items.size();
-          push_cam(cam, sb, L);
-          cum += cam_cost(cam, sb, L);
+          push_cam(cam, sb, 1);
+          cum += cam_cost(cam, sb, 1);
         }
         while (w < W) ob[++w] = (int)items.size();
         continue;
       }
-      if (L == 0) {  // whole cameras, longest first onto the least loaded warp
-        std::vector<std::pair<int64_t, int>> cams((size_t)np);
-        for (int64_t cam = 0; cam < np; ++cam) cams[cam] = {cam_cost(cam, sb, 0), (int)cam};
-        std::stable_sort(cams.begin(), cams.end(),
-                         [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& x) {
-                           return a.first > x.first;
-                         });
-        using Slot = std::pair<int64_t, int>;  // (load, warp): smallest load first, then warp
-        std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
-        for (int w = 0; w < W; ++w) heap.push({0, w});
-        std::vector<std::vector<int>> mine(W);
-        for (const auto& cc : cams) {
-          Slot s = heap.top();
-          heap.pop();
-          mine[s.second].push_back(cc.second);
-          s.first += cc.first;
-          heap.push(s);
-        }
-        int64_t tot = 0, mx = 0;
-        for (int w = 0; w < W; ++w) {
-          std::sort(mine[w].begin(), mine[w].end());
-          int64_t load = 0;
-          for (int cam : mine[w]) {
-            push_cam(cam, sb, 0);
-            load += cam_cost(cam, sb, 0);
-          }
-          hc_load[b][w] = load;
-          tot += load;
-          mx = std::max(mx, load);
-          ob[w + 1] = (int)items.size();
-        }
-        if (tot > 0) worst[0] = std::max(worst[0], (double)mx * W / (double)tot);
-        continue;
-      }
-      // W^T v: cut the item stream so that warp w ends at its share of the cumulative cost
       const size_t first = items.size();
-      int64_t tot_a = 0;
+      int64_t tot_a = 0, tot_o = 0;
       for (int64_t cam = 0; cam < np; ++cam) {
         push_cam(cam, sb, 1);
         tot_a += cam_cost(cam, sb, 1);
       }
-      std::vector<double> want(W, 1.0);
-      if (L == 2 && b > 0) {
-        int64_t tot_c = 0;
-        for (int w = 0; w < W; ++w) tot_c += hc_load[b - 1][w];
-        const double mean = (double)(tot_c + tot_a) / W;
-        for (int w = 0; w < W; ++w) want[w] = std::max(0.0, mean - (double)hc_load[b - 1][w]);
-      }
+      for (int w = 0; w < W; ++w) tot_o += other[w];
+      const double mean = (double)(tot_o + tot_a) / W;
+      std::vector<double> want(W);
       double wsum = 0.0;
-      for (int w = 0; w < W; ++w) wsum += want[w];
+      for (int w = 0; w < W; ++w) wsum += (want[w] = std::max(0.0, mean - (double)other[w]));
       if (wsum <= 0.0) {
         std::fill(want.begin(), want.end(), 1.0);
         wsum = W;
@@ -583,20 +656,27 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
           ++i;
         }
         ob[w + 1] = (int)i;
-        mx = std::max(mx, cum - start + (L == 2 && b > 0 ? (double)hc_load[b - 1][w] : 0.0));
+        mx = std::max(mx, cum - start + (double)other[w]);
       }
-      const double mean_l =
-          L == 2 && b > 0
-              ? ((double)tot_a + (double)std::accumulate(hc_load[b - 1].begin(), hc_load[b - 1].end(),
-                                                         (int64_t)0)) / W
-              : (double)tot_a / W;
-      if (mean_l > 0) worst[L] = std::max(worst[L], mx / mean_l);
+      if (mean > 0) worst[L] = std::max(worst[L], mx / mean);
     }
   }
   if (std::getenv("PV_DEBUG_BALANCE"))
-    std::fprintf(stderr, "pipe items: B=%d W=%d mode=%d cost(item=%d round=%d last=%d) worst max/mean: "
-                 "Wt %.4f  WTv %.4f  paired %.4f\n", B, W, c->bal_mode, IC, RC, LC, worst[0], worst[1],
-                 worst[2]);
+    std::fprintf(stderr,
+                 "pipe items: B=%d W=%d mode=%d cost(item=%d round=%d last=%d rfix=%d robs8=%d) worst "
+                 "max/mean: Wt %.4f  WTv %.4f  Wt+WTv %.4f  R+Wt+WTv %.4f  R+Wt %.4f\n",
+                 B, W, c->bal_mode, IC, RC, LC, c->bal_rfix, c->bal_robs8, worst[0], worst[1],
+                 worst[2], worst[3], worst[4]);
+  free_tracked(c, c->d_rslot, c->rslot_bytes);
+  free_tracked(c, c->d_roff, c->roff_bytes);
+  c->d_rslot = c->alloc<int>(std::max<size_t>(rslot.size(), 1));
+  c->d_roff = c->alloc<int>(roff.size());
+  c->rslot_bytes = std::max<size_t>(rslot.size(), 1) * sizeof(int);
+  c->roff_bytes = roff.size() * sizeof(int);
+  CK(cudaMemcpyAsync(c->d_rslot, rslot.data(), rslot.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->d_roff, roff.data(), roff.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->stream));
   free_tracked(c, c->d_items, c->items_bytes);
   free_tracked(c, c->d_item_off, c->item_off_bytes);
   c->d_items = c->alloc<int4>(items.size());
@@ -632,6 +712,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
   int64_t sn = 0;                                 // s entries so far
   c->blk_ktask.assign(B + 1, 0);
   c->blk_s.assign(B + 1, 0);
+  c->h_slot_n.clear();
   std::vector<std::vector<int>> bucket(33);
   for (int b = 0; b < B; ++b) {
     const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
@@ -656,7 +737,8 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
       kl.push_back(make_int4(l, off[l], k, (int)sn));
       for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, k, 0));
       for (int i = 0; i < k; ++i) spos[off[l] + i] = (int)(sn + i);
-      sn += k;
+      sn += (k + 3) & ~3;  // whole 128-byte lines per slot (dropped from L2 slot by slot)
+      c->h_slot_n.push_back(k);
     }
     for (int k = 32; k >= 0; --k) {
       const std::vector<int>& v = bucket[k];
@@ -673,6 +755,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
           }
         }
         sn += 32 * (int64_t)k;
+        c->h_slot_n.push_back(32 * k);
       }
     }
     if (sn >= (int64_t)INT32_MAX) throw PvError(PV_EINVAL, "too many partial slots for int32");
@@ -799,9 +882,9 @@ static void build_blocks(pv_ctx* c) {
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
+  build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
   build_pipe_items(c, seg);
   c->h_seg = seg;
-  build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
   if (c->cpart) ensure_cpart(c);   // re-blocking changes the number of warp slots
 }
 
@@ -834,6 +917,7 @@ static void alloc_buffers(pv_ctx* c) {
   c->scal = c->alloc<double>(8);
   c->flags = c->alloc<int>(F_COUNT);
   c->ticket = c->alloc<unsigned>(4);
+  c->sbar = c->alloc<unsigned>(4);
   c->ctl = c->alloc<PowerCtl>(1);
   CK(cudaHostAlloc((void**)&c->host_ctl, sizeof(PowerCtl), cudaHostAllocMapped));
   std::memset(c->host_ctl, 0, sizeof(PowerCtl));
@@ -1059,7 +1143,8 @@ static void launch_cam_last(pv_ctx* c, int c_lo, int c_hi, int first_c, int term
     } else {
       launch_cam<S, true, EP, false>(c, ep_args(cam_args(c_lo, c_hi, first_c, 0, 0, term, thr, check_stop)));
     }
-    launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, 1));
+    if (!c->skip_next_gather)
+      launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, term, thr, 1));
   } else if (!c->collective()) {
     launch_cam<S, true, EP, true>(c, ep_args(cam_args(c_lo, c_hi, first_c, 0, 1, term, thr, check_stop)));
   } else {
@@ -1134,6 +1219,50 @@ static TermGraph& term_graph(pv_ctx* c, int max_order, double thr) {
   return G;
 }
 
+// The whole term loop as one persistent cooperative kernel (pv_series.cuh): single-process
+// contexts with one warp per camera (the configuration the pipelined camera kernel covers).
+static bool series_ok(const pv_ctx* c) {
+  return c->tune.series && c->tune.cam_pipe && c->wpc == 1 && !c->collective();
+}
+template <int S>
+static void launch_series(pv_ctx* c, int max_order, double thr) {
+  const bool xm = S == 1 && c->xm_ok && c->tune.xm;
+  SeriesArgs a{};
+  a.item = c->d_items;
+  a.off = c->d_item_off;
+  a.rslot = c->d_rslot;
+  a.roff = c->d_roff;
+  a.B = c->n_blk;
+  a.W = c->pipe_W;
+  a.klist = c->d_klist;
+  a.crec = c->crec;
+  a.cs_x = xm ? c->cs_xm : c->cs_x;
+  a.cs_m1 = xm ? c->d_cs_m1 : g_null_d;
+  a.tarr = c->tarr;
+  a.sbuf = c->sbuf;
+  a.cy = c->cy;
+  a.lsys = c->lsys;
+  a.lrec = c->lrec;
+  a.cUi = c->cUi;
+  a.cx = c->cx;
+  a.ch = c->ch;
+  a.nrm = c->nrm;
+  a.ctl = c->ctl;
+  a.host_ctl = c->host_ctl_dev;
+  a.bar = c->sbar;
+  a.max_order = max_order;
+  a.thr = thr;
+  CK(cudaMemsetAsync(c->sbar, 0, 4 * sizeof(unsigned), c->stream));
+  void* args[] = {(void*)&c->g, (void*)&a, (void*)&c->coef, (void*)&c->tune};
+  const void* fn = (const void*)k_series<S, false>;
+  if constexpr (S == 1) {
+    if (xm) fn = (const void*)k_series<1, true>;
+  }
+  CK(cudaLaunchCooperativeKernel(fn, dim3(c->pipe_W / PW), dim3(PW * 32), args, PIPE_SMEM,
+                                 c->stream));
+  c->launched();
+}
+
 template <int S>
 static bool rhs_reusable(const pv_ctx* c) {
   return S == 1 && !c->last_damp_both && c->rhs_lin_id == c->lin_id && c->tune.rhs_reuse;
@@ -1169,10 +1298,13 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   // K4: t = V+ b_l for all landmarks, then y = W t over all blocks, the reduced RHS,
   // t_0 = U^-1 rhs and the gather of block 0 (a single pass; blocking does not pay here)
   const int B = c->n_blk;
+  const bool series = series_ok(c) && max_order > 0;
+  c->skip_next_gather = series;
   if (rhs_reusable<S>(c)) {  // t_0 = U^-1 rhs from the stored RHS, then block 0's gather
     if (!c->collective() && c->tune.split_last && c->wpc == 1) {
       launch_cam<S, false, EP_RHS_CACHED, false>(c, cam_args(0, 0, 0, 0, 0, 0, thr, 0));
-      launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, thr, 0));
+      if (!c->skip_next_gather)
+        launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, thr, 0));
     } else {
       launch_cam<S, false, EP_RHS_CACHED, true>(c, cam_args(0, 0, 0, 0, 1, 0, thr, 0));
     }
@@ -1181,19 +1313,26 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
     launch_cam_last<S, EP_RHS>(c, 0, B, 1, 0, thr, 0);
     mark_rhs<S>(c);
   }
+  c->skip_next_gather = false;
   c->check_launch();
   CK(cudaEventRecord(c->tev[1], c->stream));
   int launched_terms = 0;
-  if (c->tune.graph && !c->loop && max_order > 0) {  // the device-driven term loop
-    TermGraph& G = term_graph<S>(c, max_order, thr);
-    CK(cudaGraphLaunch(G.exec, c->stream));
+  if (series || (c->tune.graph && !c->loop && max_order > 0)) {  // the device-driven term loop
+    long long body_launches = 0;
+    if (series) {
+      launch_series<S>(c, max_order, thr);
+    } else {
+      TermGraph& G = term_graph<S>(c, max_order, thr);
+      CK(cudaGraphLaunch(G.exec, c->stream));
+      body_launches = G.body_launches;
+    }
     CK(cudaEventRecord(c->tev[2], c->stream));
     back_substitute_dev<S>(c);
     CK(cudaEventRecord(c->tev[3], c->stream));
     PowerCtl h;
     CK(cudaMemcpyAsync(&h, c->ctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-    c->launches += G.body_launches * h.term;  // kernels of the executed terms
+    c->launches += body_launches * h.term;  // kernels of the executed terms
     *order = h.order;
     *trunc = h.trunc;
     c->step_stage = S;
@@ -1519,6 +1658,10 @@ void pv_destroy(pv_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->host_ctl) cudaFreeHost(c->host_ctl);
+  for (int i = 0; i < 2; ++i) {
+    if (c->stage_pin[i]) cudaFreeHost(c->stage_pin[i]);
+    if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+  }
   for (auto e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : c->tev)
@@ -1557,6 +1700,9 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_SOLVE_TERMS_US] = c->solve_us[1];
   out[PV_INFO_SOLVE_BACKSUB_US] = c->solve_us[2];
   out[PV_INFO_SOLVE_TERMS_LAUNCHED] = c->solve_terms_launched;
+#ifdef PV_SER_DEBUG
+  out[PV_INFO_COUNT - 1] = c->host_ctl->pad;
+#endif
   out[PV_INFO_XM_BYTES] = (c->xm_ok && c->tune.xm && c->tune.cam_pipe && c->wpc == 1) ? 40 : 48;
   API_END(c)
 }
@@ -1619,10 +1765,16 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
     case PV_OPT_BAL_ITEM:
     case PV_OPT_BAL_ROUND:
     case PV_OPT_BAL_LAST:
+    case PV_OPT_BAL_RFIX:
+    case PV_OPT_BAL_ROBS8:
       if (value < 0 || value > 4096) throw PvError(PV_EINVAL, "balance option out of range");
       (key == PV_OPT_BALANCE ? c->bal_mode : key == PV_OPT_BAL_ITEM ? c->bal_item
-       : key == PV_OPT_BAL_ROUND ? c->bal_round : c->bal_last) = (int)value;
+       : key == PV_OPT_BAL_ROUND ? c->bal_round : key == PV_OPT_BAL_LAST ? c->bal_last
+       : key == PV_OPT_BAL_RFIX ? c->bal_rfix : c->bal_robs8) = (int)value;
       build_pipe_items(c, c->h_seg);
+      break;
+    case PV_OPT_SERIES:
+      c->tune.series = value ? 1 : 0;
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");
@@ -1641,6 +1793,85 @@ static bool lm_contiguous(const pv_ctx* c) {
   return c->n_ls == 0 || c->lm_gid.back() - c->lm_gid.front() + 1 == (int64_t)c->n_ls;
 }
 
+// Large transfers between PAGEABLE host memory and the device (the state arrays of
+// pv_set_state / pv_get_state: 143 MB at vlarge) go through two pinned staging buffers:
+// the DMA of chunk i overlaps the multi-threaded host copy of chunk i -+ 1 (first-touch
+// page faults of a fresh destination array included).  cudaMemcpy on pageable memory ran
+// at 4.6 GB/s device-to-host and 10.6 GB/s host-to-device here; pinned user memory is
+// copied directly.
+constexpr size_t STAGE_CHUNK = 8u << 20;
+static void par_memcpy(char* dst, const char* src, size_t n) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = (int)std::min<size_t>(std::min(8u, std::max(1u, hw / 2)), std::max<size_t>(1, n >> 20));
+  if (T <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t part = ((n / T) + 4095) & ~(size_t)4095;
+  for (int t = 1; t < T; ++t) {
+    const size_t o = std::min(n, part * t), e = std::min(n, part * (t + 1));
+    if (e > o) th.emplace_back([=] { std::memcpy(dst + o, src + o, e - o); });
+  }
+  std::memcpy(dst, src, std::min(n, part));
+  for (auto& x : th) x.join();
+}
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+static void stage_init(pv_ctx* c) {
+  if (c->stage_pin[0]) return;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaHostAlloc((void**)&c->stage_pin[i], STAGE_CHUNK, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+  }
+}
+// synchronous on return
+static void copy_d2h(pv_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes < 2 * STAGE_CHUNK || host_pinned(dst)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return;
+  }
+  stage_init(c);
+  const size_t nch = (bytes + STAGE_CHUNK - 1) / STAGE_CHUNK;
+  for (size_t i = 0; i <= nch; ++i) {
+    if (i < nch) {
+      const size_t o = i * STAGE_CHUNK, n = std::min(STAGE_CHUNK, bytes - o);
+      CK(cudaMemcpyAsync(c->stage_pin[i & 1], (const char*)src + o, n, cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaEventRecord(c->stage_ev[i & 1], c->stream));
+    }
+    if (i > 0) {
+      const size_t o = (i - 1) * STAGE_CHUNK, n = std::min(STAGE_CHUNK, bytes - o);
+      CK(cudaEventSynchronize(c->stage_ev[(i - 1) & 1]));
+      par_memcpy((char*)dst + o, c->stage_pin[(i - 1) & 1], n);
+    }
+  }
+}
+static void copy_h2d(pv_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes < 2 * STAGE_CHUNK || host_pinned(src)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->sync();
+    return;
+  }
+  stage_init(c);
+  const size_t nch = (bytes + STAGE_CHUNK - 1) / STAGE_CHUNK;
+  for (size_t i = 0; i < nch; ++i) {
+    const size_t o = i * STAGE_CHUNK, n = std::min(STAGE_CHUNK, bytes - o);
+    if (i >= 2) CK(cudaEventSynchronize(c->stage_ev[i & 1]));  // chunk i - 2 left the buffer
+    par_memcpy(c->stage_pin[i & 1], (const char*)src + o, n);
+    CK(cudaMemcpyAsync((char*)dst + o, c->stage_pin[i & 1], n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->stage_ev[i & 1], c->stream));
+  }
+  c->sync();
+}
+
 int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
@@ -1655,8 +1886,7 @@ int pv_set_state(pv_ctx* c, const double* cams, const double* lms) {
         for (int q = 0; q < 4; ++q) lm_local[(size_t)j * 4 + q] = lms[c->lm_gid[j] * 4 + q];
       src = lm_local.data();
     }
-    CK(cudaMemcpyAsync(c->lrec, src, sizeof(double) * 4 * c->n_ls, cudaMemcpyHostToDevice,
-                       c->stream));
+    copy_h2d(c, c->lrec, src, sizeof(double) * 4 * c->n_ls);
   }
   c->sync();
   c->lin_stage = 0;
@@ -1671,9 +1901,7 @@ static void get_state_impl(pv_ctx* c, const double* dcam, int cstride, const dou
                        12 * sizeof(double), c->n_p, cudaMemcpyDeviceToHost, c->stream));
   if (c->n_ls > 0) {
     if (lm_contiguous(c)) {
-      CK(cudaMemcpyAsync(lms + c->lm_gid.front() * 4, dlm, sizeof(double) * 4 * c->n_ls,
-                         cudaMemcpyDeviceToHost, c->stream));
-      c->sync();
+      copy_d2h(c, lms + c->lm_gid.front() * 4, dlm, sizeof(double) * 4 * c->n_ls);
     } else {
       std::vector<double> lm_local((size_t)c->n_ls * 4);
       CK(cudaMemcpyAsync(lm_local.data(), dlm, sizeof(double) * lm_local.size(),
@@ -1872,6 +2100,18 @@ int pv_schur_apply(pv_ctx* c, int stage, const double* v, double* out) {
 template <int S>
 static void op_bench_terms(pv_ctx* c, int n, float* ms) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(PowerCtl), c->stream));
+  if (series_ok(c) && !c->bench_split && n > 0) {  // n terms inside one series launch
+    CK(cudaEventRecord(c->tev[0], c->stream));
+    launch_series<S>(c, n, -1.0);
+    CK(cudaEventRecord(c->tev[3], c->stream));
+    CK(cudaEventSynchronize(c->tev[3]));
+    float d;
+    CK(cudaEventElapsedTime(&d, c->tev[0], c->tev[3]));
+    ms[0] = ms[1] = 0.f;
+    ms[2] = (float)c->n_blk;
+    ms[3] = d / n;
+    return;
+  }
   // seed s of block 0 from the current camera vector
   launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 0));
   const int B = c->n_blk;
@@ -1973,6 +2213,23 @@ int pv_debug_pipe_times(pv_ctx* c, int block, unsigned long long* t /*3*W*/, int
 }
 #endif
 
+#ifdef PV_SER_TIMING
+// diagnostic build only: barrier and per-warp timers of k_series (tools/series_times.py)
+int pv_debug_series_times(pv_ctx* c, int term, int step, unsigned long long* bar /*64*/,
+                          unsigned long long* warp /*3*W*/, int* rslot, int* roff) {
+  API_BEGIN(c)
+  CK(cudaSetDevice(c->device));
+  c->sync();
+  if (bar) CK(cudaMemcpyFromSymbol(bar, g_ser_bar, sizeof(unsigned long long) * 64));
+  if (warp) CK(cudaMemcpyFromSymbol(warp, g_ser_warp, sizeof(unsigned long long) * 3 * std::min(c->pipe_W, 8192)));
+  CK(cudaMemcpyToSymbol(g_ser_term, &term, sizeof(int)));
+  CK(cudaMemcpyToSymbol(g_ser_step, &step, sizeof(int)));
+  if (rslot) CK(cudaMemcpy(rslot, c->d_rslot, c->rslot_bytes, cudaMemcpyDeviceToHost));
+  if (roff) CK(cudaMemcpy(roff, c->d_roff, c->roff_bytes, cudaMemcpyDeviceToHost));
+  API_END(c)
+}
+#endif
+
 int pv_debug_get(pv_ctx* c, int which, double* out) {
   API_BEGIN(c)
   CK(cudaSetDevice(c->device));
@@ -2012,6 +2269,23 @@ int pv_debug_get(pv_ctx* c, int which, double* out) {
     case PV_DBG_X: {
       auto h = down(c->cx, np * 12);
       std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case 100: {  // diagnostics (tools/dbg_series*.py): y, the camera vector v, t by landmark
+      auto h = down(c->cy, np * 12);
+      std::copy(h.begin(), h.end(), out);
+      break;
+    }
+    case 101: {
+      auto h = down(c->crec, np * CREC);
+      for (size_t i = 0; i < np; ++i)
+        for (int q = 0; q < 12; ++q) out[i * 12 + q] = h[i * CREC + 12 + q];
+      break;
+    }
+    case 102: {
+      auto h = down(c->tarr, c->n_kent * 4);
+      for (size_t l = 0; l < nl; ++l)
+        for (int q = 0; q < 4; ++q) out[l * 4 + q] = h[(size_t)c->h_lpos[l] * 4 + q];
       break;
     }
     case PV_DBG_V: {

@@ -116,6 +116,45 @@ __device__ __forceinline__ void st4p(double* p, double4 v, uint64_t pol) {
                : "memory");
 }
 
+// 128-bit halves (k_series: ptxas 12.9 dropped three of the four components of a 256-bit
+// st.global.v4.f64 -- and the loads feeding them -- inside a non-inlined device function,
+// profiles/r2_series.md; two v2.f64 accesses are compiled correctly)
+__device__ __forceinline__ double4 ldg4_h(const double* p) {
+  double4 v;
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.z), "=d"(v.w) : "l"(p + 2));
+  return v;
+}
+__device__ __forceinline__ double4 ld4cg_h(const double* p, uint64_t pol) {
+  double4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol)
+               : "memory");
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.z), "=d"(v.w)
+               : "l"(p + 2), "l"(pol)
+               : "memory");
+  return v;
+}
+// coherent (L2) 256-bit load of data other CTAs wrote earlier in the same launch
+__device__ __forceinline__ double4 ld4cg(const double* p, uint64_t pol) {
+  double4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p), "l"(pol)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st4p_h(double* p, double4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p + 2), "d"(v.z),
+               "d"(v.w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
@@ -363,7 +402,7 @@ __device__ __forceinline__ void basis_apply(const double* h, const double* t, do
 #pragma unroll
   for (int i = 1; i < N; ++i) d = fma(h[i], t[i - 1], d);
 #pragma unroll
-  for (int i = 0; i < N; ++i) out[i] = (i == 0 ? 0.0 : t[i - 1]) - 2.0 * h[i] * d;
+  for (int i = 0; i < N; ++i) out[i] = fma(-2.0 * h[i], d, i == 0 ? 0.0 : t[i - 1]);
 }
 
 // out (N-1) = B^T s  with s (N)
@@ -373,7 +412,7 @@ __device__ __forceinline__ void basis_apply_t(const double* h, const double* s, 
 #pragma unroll
   for (int i = 0; i < N; ++i) d = fma(h[i], s[i], d);
 #pragma unroll
-  for (int i = 1; i < N; ++i) out[i - 1] = s[i] - 2.0 * h[i] * d;
+  for (int i = 1; i < N; ++i) out[i - 1] = fma(-2.0 * h[i], d, s[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -441,9 +480,11 @@ __device__ inline bool pinv_sym3(const double* a6, double rel_tol, double* out6)
 }
 
 __device__ __forceinline__ void sym3_apply(const double* a6, const double* v, double* o) {
-  o[0] = a6[0] * v[0] + a6[1] * v[1] + a6[2] * v[2];
-  o[1] = a6[1] * v[0] + a6[3] * v[1] + a6[4] * v[2];
-  o[2] = a6[2] * v[0] + a6[4] * v[1] + a6[5] * v[2];
+  // explicit fma chains: the same bits in every kernel that inlines this (implicit contraction
+  // is chosen per inlining context and differed between k_lm_reduce and k_series)
+  o[0] = fma(a6[2], v[2], fma(a6[1], v[1], a6[0] * v[0]));
+  o[1] = fma(a6[4], v[2], fma(a6[3], v[1], a6[1] * v[0]));
+  o[2] = fma(a6[5], v[2], fma(a6[4], v[1], a6[2] * v[0]));
 }
 
 __device__ __forceinline__ double damp_diag(double d, double lam) {

@@ -41,6 +41,7 @@ struct Tune {
   int rhs_reuse;     // reuse the reduced RHS across solves of one POSE_ONLY linearization
   int cost_cs;       // cost over the camera-sorted segments (k_cost_cs) instead of k_cost
   int graph;         // power-series term loop as a CUDA graph WHILE node (no host round trips)
+  int series;        // the whole power series as one persistent cooperative kernel (pv_series.cuh)
 };
 
 enum { F_INVALID_Z = 0, F_ZERO_NORM = 1, F_SINGULAR_U = 2, F_N_DEGEN = 3, F_N_RANKDEF = 4,
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       if (STAGE == 2) {
         const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
         const double hu = warp_sum(h * u);
-        const double pr = u - 2.0 * h * hu;
+        const double pr = fma(-2.0 * h, hu, u);
         u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
         if (lane >= 11) u = 0.0;
       }
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
       if (STAGE == 2) {  // project y (12) -> tangent (11)
         h = (row && valid) ? ch[(size_t)cam * 12 + lane] : 0.0;
         const double hu = warp_sum(h * u);
-        const double pr = u - 2.0 * h * hu;
+        const double pr = fma(-2.0 * h, hu, u);
         u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
         if (lane >= 11) u = 0.0;
       }
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
         const double tprev = __shfl_sync(PV_FULL, t, (lane + 31) & 31);
         const double e = (lane >= 1 && lane < 12) ? tprev : 0.0;
         const double hd = warp_sum(h * e);
-        v = e - 2.0 * h * hd;
+        v = fma(-2.0 * h, hd, e);
       }
       if (row && valid) crec[(size_t)cam * CREC + 12 + lane] = v;  // for the later blocks
       if (row) gv[grp][lane] = v;
@@ -545,7 +546,7 @@ __global__ void k_project_y(int n_p, const double* __restrict__ cy, const double
   if (STAGE == 2) {
     const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
     const double hu = warp_sum(h * u);
-    const double pr = u - 2.0 * h * hu;
+    const double pr = fma(-2.0 * h, hu, u);
     u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
     if (lane >= 11) u = 0.0;
   }
@@ -563,20 +564,22 @@ struct LmPre {  // per-landmark inputs of the landmark epilogue, prefetched befo
   double4 va, vb, bl, x;
 };
 
-template <int STAGE, int MODE>
+// H: 128-bit accesses (k_series, see ldg4_h)
+template <int STAGE, int MODE, bool H = false>
 __device__ __forceinline__ LmPre lm_prefetch(int l, int kp, const double* __restrict__ lrec,
                                              const double* __restrict__ lsys,
                                              const double* __restrict__ lbl) {
   LmPre p;
-  p.va = ldg4(lsys + (size_t)kp * LSYS);
-  p.vb = ldg4(lsys + (size_t)kp * LSYS + 4);
-  p.x = (STAGE == 2 || MODE == LR_BACKSUB) ? ldg4(lrec + (size_t)l * LREC)
-                                           : make_double4(0.0, 0.0, 0.0, 1.0);
+  p.va = H ? ldg4_h(lsys + (size_t)kp * LSYS) : ldg4(lsys + (size_t)kp * LSYS);
+  p.vb = H ? ldg4_h(lsys + (size_t)kp * LSYS + 4) : ldg4(lsys + (size_t)kp * LSYS + 4);
+  p.x = (STAGE == 2 || MODE == LR_BACKSUB)
+            ? (H ? ldg4_h(lrec + (size_t)l * LREC) : ldg4(lrec + (size_t)l * LREC))
+            : make_double4(0.0, 0.0, 0.0, 1.0);
   p.bl = MODE != LR_TERM ? ldg4(lbl + (size_t)l * 4) : make_double4(0.0, 0.0, 0.0, 0.0);
   return p;
 }
 
-template <int STAGE, int MODE>
+template <int STAGE, int MODE, bool H = false>
 __device__ __forceinline__ void lm_finish(int l, int kp, const double (&acc)[4], const LmPre& p,
                                           double* __restrict__ tarr, double* __restrict__ ldl,
                                           double* __restrict__ tlm, int* __restrict__ flags,
@@ -600,13 +603,18 @@ __device__ __forceinline__ void lm_finish(int l, int kp, const double (&acc)[4],
   if (MODE != LR_BACKSUB) {
     double t[3];
     sym3_apply(vp, s3, t);
+    double4 tv;
     if (STAGE == 1) {
-      st4p(tarr + (size_t)kp * 4, make_double4(t[0], t[1], t[2], 0.0), pt);
+      tv = make_double4(t[0], t[1], t[2], 0.0);
     } else {
       double t4[4];
       basis_apply<4>(h, t, t4);
-      st4p(tarr + (size_t)kp * 4, make_double4(t4[0], t4[1], t4[2], t4[3]), pt);
+      tv = make_double4(t4[0], t4[1], t4[2], t4[3]);
     }
+    if (H)
+      st4p_h(tarr + (size_t)kp * 4, tv, pt);
+    else
+      st4p(tarr + (size_t)kp * 4, tv, pt);
     return;
   }
   double q[3] = {s3[0] + p.bl.x, s3[1] + p.bl.y, s3[2] + p.bl.z};

@@ -338,7 +338,7 @@ __device__ __forceinline__ void store_camera_vector(double* __restrict__ crec,
     const double pprev = __shfl_sync(PV_FULL, p, (lane + 31) & 31);
     const double e = (lane >= 1 && lane < 12) ? pprev : 0.0;
     const double hd = warp_sum(h * e);
-    v = e - 2.0 * h * hd;
+    v = fma(-2.0 * h, hd, e);
   }
   if (lane < 12) crec[(size_t)cam * CREC + 12 + lane] = v;
 }
@@ -412,7 +412,7 @@ __global__ void k_pcg_curv(int n_p, int it, const double* __restrict__ cy,
     if (STAGE == 2) {  // raw 12 -> tangent 11
       const double h = lane < 12 ? ch[(size_t)cam * 12 + lane] : 0.0;
       const double hu = warp_sum(h * u);
-      const double pr = u - 2.0 * h * hu;
+      const double pr = fma(-2.0 * h, hu, u);
       u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
     }
     const double p = lane < D ? v.p[(size_t)cam * 12 + lane] : 0.0;

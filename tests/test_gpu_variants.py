@@ -37,9 +37,15 @@ def test_pipe_matches_k_cam(pv, stage):
     st = pv.ProjectiveState(z["cams"], z["lms"]) if stage == 1 else \
         pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"])
     outs = []
+    # the series kernel (default), the term graph, the host term loop, the full (x, m)
+    # stream, and the contiguous work-list balance, all against k_cam
     variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
                 [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_XM, 0)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_GRAPH, 0)])
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_XM, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_GRAPH, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_BALANCE, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_BALANCE, 0)])
     for knobs in variants:
         dp = _ctx(pv, z, knobs)
         info = dp.info()
@@ -116,8 +122,9 @@ def test_pipe_long_work_lists_large(pv, stage):
     dp.damp(1e-4, stage == 2)
     assert dp.info()["warps_per_cam"] == 1 and dp.info()["blocks"] > 10
     out = []
-    for v in (0, 1):
+    for v, series in ((0, 0), (1, 0), (1, 1)):  # k_cam, launch per block, series kernel
         dp.set_option(_lib.PV_OPT_CAM_PIPE, v)
+        dp.set_option(_lib.PV_OPT_SERIES, series)
         dp.linearize(stage)
         dp.damp(1e-4, stage == 2)
         order, trunc = dp.power_solve(4, 0.0)
