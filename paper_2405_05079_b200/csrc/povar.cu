@@ -205,7 +205,7 @@ struct pv_ctx {
          *ppart = nullptr;
   PowerCtl* host_ctl_dev = nullptr;
 
-  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+  Tune tune{0, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 0};
   int64_t last_fallbacks = 0;  // landmarks that took the exact Givens path in the last re-solve
   int lin_stage = 0;
   bool vp_cached = false;  // V+ valid for POSE_ONLY damping of the current linearization
@@ -1248,7 +1248,6 @@ static void launch_series(pv_ctx* c, int max_order, double thr) {
   a.ch = c->ch;
   a.nrm = c->nrm;
   a.ctl = c->ctl;
-  a.host_ctl = c->host_ctl_dev;
   a.bar = c->sbar;
   a.max_order = max_order;
   a.thr = thr;

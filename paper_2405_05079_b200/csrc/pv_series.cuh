@@ -2,20 +2,22 @@
 // cooperative kernel: every term's landmark reduces, camera passes, U^-1 epilogue and stop
 // test run inside it, separated by grid barriers instead of kernel boundaries.
 //
-// Why (profiles/r2_series.md): with one launch per landmark block and pass a term is 26
+// Why (profiles/r2_series.md; measured outcome: no gain, opt-in): with one launch per landmark block and pass a term is 26
 // dependent launches of 20-70 us at vlarge; the HC-only + HA-only launches of a block take
 // ~8.5 us longer than the fused one, i.e. every launch boundary costs ~8 us of drain, launch
 // latency and pipeline refill -- ~0.2 ms of a 1.06 ms term.
 //
 // Schedule of one term over B landmark blocks (s, t, y as in pv_pipe.cuh; every step ends
-// with a grid barrier, B + 3 per term):
+// with a grid barrier, B + 2 per term):
 //
 //   step -2:  W^T v (0)
 //   step -1:  R(0), W^T v (1)
 //   step  k:  R(k+1), W t (k), W^T v (k+2)           k = 0 .. B-1 (out-of-range parts dropped)
-//   epilogue: v = U^-1 y, x += v, norms (warp per camera); the LAST CTA to arrive at the
-//             barrier sums the norms in the order of k_cam's last CTA and takes the stop
-//             decision before it releases the others.
+//
+// In step B-1 the warp that completes a camera's y runs the epilogue for it at once (v = U^-1 y,
+// x += v, norms, y still in registers), and the LAST CTA to arrive at that step's barrier sums
+// the norms in the order of k_cam's last CTA and takes the stop decision before it releases
+// the others.
 //
 // R(b) is the landmark reduce t_j = V+_j sum_i s_ij of block b (k_lm_reduce's slots, here
 // from a per-warp slot list); inside a step each warp first reduces its slots -- so the
@@ -59,7 +61,6 @@ struct SeriesArgs {
   const double* ch;
   double* nrm;
   PowerCtl* ctl;
-  volatile PowerCtl* host_ctl;
   unsigned* bar;  // [0] arrivals (monotonic within a launch), [1] released generation
   int max_order;
   double thr;
@@ -190,54 +191,52 @@ __device__ PV_SER_FN void series_reduce_list(const SeriesArgs& a, int r0, int r1
   }
 }
 
-// epilogue of a term (k_cam EP_TERM): v = U^-1 y, x += v, norms.  Two cameras per warp, one
-// per half-warp (lanes 0-11 / 16-27 hold the 12 components); the 16-lane butterflies add
-// what k_cam's 32-lane ones add (there the upper half holds zeros), so the bits are the same.
+// epilogue of a term for one camera (k_cam EP_TERM, one warp): v = U^-1 y, x += v, norms.
+// Called by the warp that finishes the camera's y in the term's last W t pass, with y in
+// lanes 0-11 (u): no separate pass over the cameras, and no re-read of y.
 template <int STAGE>
-__device__ PV_SER_FN void series_epilogue(const SeriesArgs& a, int n_p, int cam0, int lane) {
+__device__ PV_SER_FN void series_epilogue(const SeriesArgs& a, int cam, int lane, double u) {
   constexpr int D = STAGE == 1 ? 12 : 11;
-  const int hl = lane & 15;
-  const int cam = cam0 + (lane >> 4);
-  const bool valid = cam < n_p;
-  const bool row = hl < 12 && valid;
-  auto half_sum = [](double v) {
-#pragma unroll
-    for (int d = 8; d > 0; d >>= 1) v += __shfl_xor_sync(PV_FULL, v, d);
-    return v;
-  };
-  double u = row ? __ldcg(a.cy + (size_t)cam * 12 + hl) : 0.0;
+  const bool row = lane < 12;
+  if (!row) u = 0.0;
   double h = 0.0;
   if (STAGE == 2) {  // project y (12) -> tangent (11)
-    h = row ? a.ch[(size_t)cam * 12 + hl] : 0.0;
-    const double hu = half_sum(h * u);
+    h = row ? a.ch[(size_t)cam * 12 + lane] : 0.0;
+    const double hu = warp_sum(h * u);
     const double pr = fma(-2.0 * h, hu, u);
-    u = __shfl_sync(PV_FULL, pr, (hl + 1) & 15, 16);
-    if (hl >= 11) u = 0.0;
+    u = __shfl_sync(PV_FULL, pr, (lane + 1) & 31);
+    if (lane >= 11) u = 0.0;
   }
   const double vin = u;
   double t = 0.0;
-  const double* Ui = a.cUi + (size_t)(valid ? cam : 0) * 144 + (hl < D ? hl : 0) * 12;
+  const double* Ui = a.cUi + (size_t)cam * 144 + (lane < D ? lane : 0) * 12;
+  const double xold = lane < D ? a.cx[(size_t)cam * 12 + lane] : 0.0;  // in flight with U^-1
+  double ui[12];  // the row of U^-1, all loads in flight before the shuffle chain
+#pragma unroll
+  for (int kk = 0; kk < 12; ++kk) ui[kk] = (lane < D && kk < D) ? __ldg(Ui + kk) : 0.0;
 #pragma unroll
   for (int kk = 0; kk < 12; ++kk) {
-    const double vk = __shfl_sync(PV_FULL, vin, kk, 16);
-    if (valid && hl < D && kk < D) t = fma(Ui[kk], vk, t);
+    const double vk = __shfl_sync(PV_FULL, vin, kk);
+    if (lane < D && kk < D) t = fma(ui[kk], vk, t);
   }
   double xr = 0.0;
-  if (valid && hl < D) {
-    xr = a.cx[(size_t)cam * 12 + hl] + t;
-    a.cx[(size_t)cam * 12 + hl] = xr;
+  if (lane < D) {
+    xr = xold + t;
+    a.cx[(size_t)cam * 12 + lane] = xr;
   }
   double v = t;
   if (STAGE == 2) {  // v = B t (11 -> 12)
-    const double tprev = __shfl_sync(PV_FULL, t, (hl + 15) & 15, 16);
-    const double e = (hl >= 1 && hl < 12) ? tprev : 0.0;
-    const double hd = half_sum(h * e);
+    const double tprev = __shfl_sync(PV_FULL, t, (lane + 31) & 31);
+    const double e = (lane >= 1 && lane < 12) ? tprev : 0.0;
+    const double hd = warp_sum(h * e);
     v = fma(-2.0 * h, hd, e);
   }
-  if (row) a.crec[(size_t)cam * CREC + 12 + hl] = v;
-  const double tn = half_sum(hl < D ? t * t : 0.0);
-  const double xn = half_sum(hl < D ? xr * xr : 0.0);
-  if (hl == 0 && valid) {
+  // the camera records of this step's other W t items are read concurrently (TMA), but only
+  // their P half is used there; the next W^T v pass reads v after the grid barrier
+  if (row) a.crec[(size_t)cam * CREC + 12 + lane] = v;
+  const double tn = warp_sum(lane < D ? t * t : 0.0);
+  const double xn = warp_sum(lane < D ? xr * xr : 0.0);
+  if (lane == 0) {
     a.nrm[2 * (size_t)cam] = tn;
     a.nrm[2 * (size_t)cam + 1] = xn;
   }
@@ -331,6 +330,13 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
         const int s = (gbase + n_prod) % PD;
         unsigned char* slot = wsm + s * PSLOT;
         PV_CHECK(cam >= 0 && cam < g.n_p && n >= 0 && n <= PCH && o >= 0 && o + n <= g.n_o);
+        if (hb == B - 1 && (fl & (PF_HA | PF_LAST)) == PF_LAST && lane < 10) {
+          // this item completes a camera's y in the term's last block: its epilogue follows
+          // two items later; pull U^-1 (9 lines) and x (1 line) into L2 now
+          const char* pa = lane < 9 ? reinterpret_cast<const char*>(a.cUi + (size_t)cam * 144) + 128 * lane
+                                    : reinterpret_cast<const char*>(a.cx + (size_t)cam * 12);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+        }
         if (lane == 0) {
 #if PV_PIPE_FENCE
           fence_proxy_async();
@@ -441,10 +447,13 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
           }
           if (fl & PF_LAST) {  // camera done: fixed-order warp reduction, write y
             const double mine = warp_reduce12_lane(acc, lane);
+            double yv = 0.0;
             if (lane < 12) {
               double* yp = a.cy + (size_t)cam * 12 + lane;
-              *yp = first_c ? mine : __ldcg(yp) + mine;
+              yv = first_c ? mine : __ldcg(yp) + mine;
+              *yp = yv;
             }
+            if (hb == B - 1) series_epilogue<STAGE>(a, cam, lane, yv);  // y is complete
 #pragma unroll
             for (int i = 0; i < 12; ++i) acc[i] = 0.0;
           }
@@ -479,69 +488,86 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
 #ifdef PV_SER_TIMING
       if (tme) SER_T(g_ser_warp[3 * gw + 2]);
 #endif
-      grid_sync(a.bar, phase, &s_last, nothing);
+      // the last step's barrier also carries the stop decision: the LAST CTA to arrive sums the
+      // norms (k_cam's order: 256 strided partial sums, a butterfly per 32, then 8 in order)
+      // and decides (solvers.py:140-149) before it releases the others
+      if (step < B - 1) {
+        grid_sync(a.bar, phase, &s_last, nothing);
+      } else {
+        grid_sync(a.bar, phase, &s_last, [&] {
+          // 256 strided chains (virtual thread vt sums cameras vt, vt + 256, ... in order); a warp
+          // walks its up to three virtual warps together, eight loads of each in flight
+          {
+            constexpr int NVW = (8 + PW - 1) / PW;
+            double ra[NVW][2];
+#pragma unroll
+            for (int q = 0; q < NVW; ++q) ra[q][0] = ra[q][1] = 0.0;
+            const double2* nr = reinterpret_cast<const double2*>(a.nrm);
+            for (int i0 = 0; i0 < g.n_p; i0 += 8 * 256) {
+              double2 v[NVW][8];
+#pragma unroll
+              for (int q = 0; q < NVW; ++q) {
+                const int vw = warp + q * PW;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const int i = i0 + u * 256 + vw * 32 + lane;
+                  v[q][u] = (vw < 8 && i < g.n_p) ? __ldcg(nr + i) : make_double2(0.0, 0.0);
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < NVW; ++q) {
+                const int vw = warp + q * PW;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const int i = i0 + u * 256 + vw * 32 + lane;
+                  if (vw < 8 && i < g.n_p) {  // added in camera order; skipped terms add nothing
+                    ra[q][0] += v[q][u].x;
+                    ra[q][1] += v[q][u].y;
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < NVW; ++q) {
+              const int vw = warp + q * PW;
+              if (vw < 8) {  // warp-uniform
+                double r2[2] = {ra[q][0], ra[q][1]};
+                warp_reduce_all(r2);
+                if (lane == 0) {
+                  s_rr[0][vw] = r2[0];
+                  s_rr[1][vw] = r2[1];
+                }
+              }
+            }
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            double TN2 = 0.0, XN2 = 0.0;
+            for (int q = 0; q < 8; ++q) {
+              TN2 += s_rr[0][q];
+              XN2 += s_rr[1][q];
+            }
+            const double TN = sqrt(TN2), XN = sqrt(XN2);
+            PowerCtl c = *a.ctl;
+            const double ratio = XN > 0.0 ? TN / XN : 0.0;
+            c.trunc = ratio;
+            c.term = term;
+            if (ratio <= a.thr) {
+              c.order = term - 1;
+              c.stopped = 1;
+            } else {
+              c.order = term;
+            }
+            c.xnorm = XN;
+            c.tnorm = TN;
+            *a.ctl = c;  // the host reads it after the launch (no mapped mirror: nobody polls)
+          }
+        });
+      }
 #ifdef PV_SER_TIMING
       if (term == g_ser_term && threadIdx.x == 0 && blockIdx.x == 0) SER_T(g_ser_bar[step + 3]);
 #endif
     }
-
-    // ---- epilogue (k_cam EP_TERM, one warp per camera): v = U^-1 y, x += v, norms
-    for (int cam0 = 2 * gw; cam0 < g.n_p; cam0 += 2 * W) series_epilogue<STAGE>(a, g.n_p, cam0, lane);
-    // ---- the last CTA to arrive sums the norms (k_cam's order: 256 strided partial sums,
-    // a butterfly per 32, then 8 in order) and takes the stop decision (solvers.py:140-149)
-    grid_sync(a.bar, phase, &s_last, [&] {
-      for (int vw = warp; vw < 8; vw += PW) {
-        double ra[2] = {0.0, 0.0};
-        int i = vw * 32 + lane;
-        for (; i + 768 < g.n_p; i += 1024) {  // four loads in flight, added in order
-          const double2 q0 = __ldcg(reinterpret_cast<const double2*>(a.nrm) + i),
-                        q1 = __ldcg(reinterpret_cast<const double2*>(a.nrm) + i + 256),
-                        q2 = __ldcg(reinterpret_cast<const double2*>(a.nrm) + i + 512),
-                        q3 = __ldcg(reinterpret_cast<const double2*>(a.nrm) + i + 768);
-          ra[0] = ((ra[0] + q0.x) + q1.x) + q2.x + q3.x;
-          ra[1] = ((ra[1] + q0.y) + q1.y) + q2.y + q3.y;
-        }
-        for (; i < g.n_p; i += 256) {
-          const double2 q = __ldcg(reinterpret_cast<const double2*>(a.nrm) + i);
-          ra[0] += q.x;
-          ra[1] += q.y;
-        }
-        warp_reduce_all(ra);
-        if (lane == 0) {
-          s_rr[0][vw] = ra[0];
-          s_rr[1][vw] = ra[1];
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double TN2 = 0.0, XN2 = 0.0;
-        for (int q = 0; q < 8; ++q) {
-          TN2 += s_rr[0][q];
-          XN2 += s_rr[1][q];
-        }
-        const double TN = sqrt(TN2), XN = sqrt(XN2);
-        PowerCtl c = *a.ctl;
-        const double ratio = XN > 0.0 ? TN / XN : 0.0;
-        c.trunc = ratio;
-        c.term = term;
-        if (ratio <= a.thr) {
-          c.order = term - 1;
-          c.stopped = 1;
-        } else {
-          c.order = term;
-        }
-        c.xnorm = XN;
-        c.tnorm = TN;
-        *a.ctl = c;
-        a.host_ctl->order = c.order;
-        a.host_ctl->term = c.term;
-        a.host_ctl->trunc = c.trunc;
-        a.host_ctl->xnorm = c.xnorm;
-        a.host_ctl->tnorm = c.tnorm;
-        __threadfence_system();
-        a.host_ctl->stopped = c.stopped;
-      }
-    });
 #ifdef PV_SER_TIMING
     if (term == g_ser_term && threadIdx.x == 0 && blockIdx.x == 0) SER_T(g_ser_bar[B + 3]);
 #endif

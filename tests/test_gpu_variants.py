@@ -37,15 +37,15 @@ def test_pipe_matches_k_cam(pv, stage):
     st = pv.ProjectiveState(z["cams"], z["lms"]) if stage == 1 else \
         pv.ProjectiveState(z["s2_cams0"], z["s2_lms0"])
     outs = []
-    # the series kernel (default), the term graph, the host term loop, the full (x, m)
-    # stream, and the contiguous work-list balance, all against k_cam
+    # the term graph (default), the host term loop, the one-kernel series (k_series), the
+    # full (x, m) stream, and the contiguous work-list balance, all against k_cam
     variants = ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
                 [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_XM, 0)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_XM, 0)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_GRAPH, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_GRAPH, 0)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 1)],
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 1), (_lib.PV_OPT_XM, 0)],
                 [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_BALANCE, 0)],
-                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 0), (_lib.PV_OPT_BALANCE, 0)])
+                [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 1), (_lib.PV_OPT_BALANCE, 0)])
     for knobs in variants:
         dp = _ctx(pv, z, knobs)
         info = dp.info()
@@ -89,10 +89,11 @@ def test_compact_stream_falls_back_when_w_is_not_one(pv):
     np.testing.assert_array_equal(outs[0].landmark_update, outs[1].landmark_update)
 
 
-def test_pipe_lm_trace_matches_reference(pv):
+@pytest.mark.parametrize("series", [0, 1])
+def test_pipe_lm_trace_matches_reference(pv, series):
     from paper_2405_05079_b200 import _lib
     z = golden("tiny_lm.npz")
-    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, 1)])
+    dp = _ctx(pv, z, [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, series)])
     st = pv.ProjectiveState(z["cams"], z["lms"])
     _, trace = pv.lm_minimize(dp.problem, st, 1, pv.SolverConfig(max_outer_iterations=20),
                               dp=dp)

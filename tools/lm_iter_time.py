@@ -1,6 +1,6 @@
 """Time stage-1 LM iterations exactly as bench.py's `value` loop does (3 warm-up + K timed,
 CUDA events on the library stream), for A/B of builds: PV_LIB_PATH=... python
-tools/lm_iter_time.py [config] [K]"""
+tools/lm_iter_time.py [config] [K] [PV_OPT_x=v ...]"""
 import math
 import os
 import sys
@@ -18,6 +18,10 @@ K = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 cfg = synth.CONFIGS[name]
 problem, _ = synth.make_problem(name, 0)
 dp = pv.DeviceProblem(problem, 0.1)
+from paper_2405_05079_b200 import _lib  # noqa: E402
+for kv in sys.argv[3:]:  # e.g. PV_OPT_SERIES=0
+    k, v = kv.split("=")
+    dp.set_option(getattr(_lib, k), int(v))
 stream = torch.cuda.ExternalStream(dp.stream_handle)
 scfg = pv.SolverConfig(max_outer_iterations=1, max_power_order=cfg.max_power_order,
                        function_tolerance=1e-300)
@@ -63,5 +67,5 @@ for _ in range(K):
 e1.record(stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / K
-print(f"{os.environ.get('PV_LIB_PATH', 'default')}: {ms:.3f} ms/iteration, orders {orders}, "
+print(f"{os.environ.get('PV_LIB_PATH', 'default')} {' '.join(sys.argv[3:])}: {ms:.3f} ms/iteration, orders {orders}, "
       f"accepted {sum(acc)}/{K}, cost {f!r}")
