@@ -1699,9 +1699,6 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_SOLVE_TERMS_US] = c->solve_us[1];
   out[PV_INFO_SOLVE_BACKSUB_US] = c->solve_us[2];
   out[PV_INFO_SOLVE_TERMS_LAUNCHED] = c->solve_terms_launched;
-#ifdef PV_SER_DEBUG
-  out[PV_INFO_COUNT - 1] = c->host_ctl->pad;
-#endif
   out[PV_INFO_XM_BYTES] = (c->xm_ok && c->tune.xm && c->tune.cam_pipe && c->wpc == 1) ? 40 : 48;
   API_END(c)
 }
@@ -2268,23 +2265,6 @@ int pv_debug_get(pv_ctx* c, int which, double* out) {
     case PV_DBG_X: {
       auto h = down(c->cx, np * 12);
       std::copy(h.begin(), h.end(), out);
-      break;
-    }
-    case 100: {  // diagnostics (tools/dbg_series*.py): y, the camera vector v, t by landmark
-      auto h = down(c->cy, np * 12);
-      std::copy(h.begin(), h.end(), out);
-      break;
-    }
-    case 101: {
-      auto h = down(c->crec, np * CREC);
-      for (size_t i = 0; i < np; ++i)
-        for (int q = 0; q < 12; ++q) out[i * 12 + q] = h[i * CREC + 12 + q];
-      break;
-    }
-    case 102: {
-      auto h = down(c->tarr, c->n_kent * 4);
-      for (size_t l = 0; l < nl; ++l)
-        for (int q = 0; q < 4; ++q) out[l * 4 + q] = h[(size_t)c->h_lpos[l] * 4 + q];
       break;
     }
     case PV_DBG_V: {
