@@ -695,8 +695,8 @@ static void build_pipe_items(pv_ctx* c, const std::vector<int>& seg) {
 // re-solve, and the layout of the per-observation partials s.  Per landmark block, the
 // landmarks are bucketed by track length k and laid out as 32-entry warp slots of
 // {landmark, first landmark-sorted observation, k, s position}: a short slot holds up to
-// 32 landmarks of equal k <= 32 (one lane each; unused lanes have landmark -1); a long
-// landmark (k > 32) fills a slot alone.  Longest first, so a grid's tail is made of short
+// 32 landmarks of equal k <= KSHORT (one lane each; unused lanes have landmark -1); a long
+// landmark (k > KSHORT) fills a slot alone.  Longest first, so a grid's tail is made of short
 // slots.  The partials s of a short slot are interleaved -- observation i of lane q at
 // base + 32 i + q -- so the reduce's k-step walk reads 1 KB contiguous per warp load; a
 // long landmark's partials are contiguous.  cs_ls holds the landmark-sorted position of
@@ -713,7 +713,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
   c->blk_ktask.assign(B + 1, 0);
   c->blk_s.assign(B + 1, 0);
   c->h_slot_n.clear();
-  std::vector<std::vector<int>> bucket(33);
+  std::vector<std::vector<int>> bucket(KSHORT + 1);
   for (int b = 0; b < B; ++b) {
     const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
     const int l0 = t0 < c->n_tasks ? c->h_task_desc[4 * t0 + 2] : c->n_ls;
@@ -722,7 +722,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
     for (auto& v : bucket) v.clear();
     for (int l = l0; l < l1; ++l) {
       const int k = off[l + 1] - off[l];
-      if (k > 32)
+      if (k > KSHORT)
         longs.emplace_back(k, l);
       else
         bucket[k].push_back(l);
@@ -740,7 +740,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
       sn += (k + 3) & ~3;  // whole 128-byte lines per slot (dropped from L2 slot by slot)
       c->h_slot_n.push_back(k);
     }
-    for (int k = 32; k >= 0; --k) {
+    for (int k = KSHORT; k >= 0; --k) {
       const std::vector<int>& v = bucket[k];
       for (size_t i = 0; i < v.size(); i += 32) {
         const int n = (int)std::min<size_t>(32, v.size() - i);

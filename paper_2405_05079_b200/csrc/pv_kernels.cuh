@@ -25,6 +25,15 @@ constexpr int LREC = 4;   // landmark record: x (4)
 constexpr int LSYS = 8;   // V+ (6) | degenerate (1) | pad
 constexpr int LINP = 90;  // camera linearization: U upper (78) | b_p (12)
 constexpr int FT = 256;   // threads of a camera CTA
+// landmark warp slots (build_ktasks, povar.cu): a landmark with at most KSHORT observations
+// shares a slot with up to 31 others of the same track length, one lane each walking its
+// observations serially; a longer one fills a slot alone and is walked by the whole warp.
+// 64: vlarge term 1.071 -> 1.056 ms, LM iteration 19.90 -> 19.66 ms against 32 (48: 1.068 /
+// 19.78; 96: 1.117 / 20.59 -- a 96-step serial slot is too long for a ~20 us launch)
+#ifndef PV_KSHORT
+#define PV_KSHORT 64
+#endif
+constexpr int KSHORT = PV_KSHORT;
 
 // runtime tuning of the term kernels (pv_set_option): on-chip staging capacity
 // and L2 eviction priorities (0 normal, 1 evict_first, 2 evict_last)
@@ -643,9 +652,9 @@ __device__ __forceinline__ void lm_finish(int l, int kp, const double (&acc)[4],
 }
 
 // Landmark half of a term.  Work unit (built by build_ktasks, povar.cu): up to 32
-// landmarks of one block with the same track length k <= 32, one lane per landmark,
+// landmarks of one block with the same track length k <= KSHORT, one lane per landmark,
 // each lane summing its k partials s_ij serially (k is warp-uniform: no divergence,
-// no shuffles, ~5 instructions per observation); a landmark with k > 32 is a unit of
+// no shuffles, ~5 instructions per observation); a landmark with k > KSHORT is a unit of
 // its own, reduced by the whole warp (coalesced, fixed-order tree).  Deterministic.
 
 template <int STAGE, int MODE>
@@ -709,7 +718,7 @@ __global__ void __launch_bounds__(256, PV_LR_MINB) k_lm_reduce(const int4* __res
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
   const int4 e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k}
   const int k = e.z;                                      // warp-uniform
-  if (k > 32) {
+  if (k > KSHORT) {
     Task t;
     t.l0 = __shfl_sync(PV_FULL, e.x, 0);
     t.o0 = __shfl_sync(PV_FULL, e.w, 0);  // contiguous partials
@@ -852,7 +861,7 @@ __device__ __forceinline__ void lin_lm_finish(int l, const double (&acc)[9],
 }
 
 // Same, over the k-bucketed warp slots of the landmark reduce (build_ktasks): one lane
-// per landmark walks its k <= 32 observations serially (no shuffle trees; the landmark's
+// per landmark walks its k <= KSHORT observations serially (no shuffle trees; the landmark's
 // Householder basis is built once per lane); a long landmark's slot is reduced by the
 // whole warp.  The per-landmark sums run in a different (fixed) order than k_lin_lm's.
 template <int STAGE>
@@ -872,7 +881,7 @@ __global__ void __launch_bounds__(256) k_lin_lm_slots(Graph g, const int4* __res
 #pragma unroll
   for (int i = 0; i < 9; ++i) acc[i] = 0.0;
   double h[4] = {0.0, 0.0, 0.0, 0.0};
-  if (kk > 32) {
+  if (kk > KSHORT) {
     const int l = __shfl_sync(PV_FULL, e.x, 0), o0 = __shfl_sync(PV_FULL, e.y, 0);
     const double4 x = ldg4(lrec + (size_t)l * LREC);
     if (STAGE == 2) {
@@ -1752,12 +1761,12 @@ __global__ void __launch_bounds__(64, 8) k_resolve(Graph g, const double* __rest
 }
 
 // Landmark re-solve, lane-per-landmark form (the same k-bucketed warp slots as the
-// landmark reduce): each lane owns one landmark with k <= 32 observations and walks them
+// landmark reduce): each lane owns one landmark with k <= KSHORT observations and walks them
 // serially -- pass 1 builds [A^T A | A^T c] (no shuffles), the lane solves (every lane
 // busy), an ill-conditioned landmark repeats the walk for the CholeskyQR2 pass, and a
 // last walk evaluates the stage-1 cost at the new coordinates.  The observation rows are
 // rebuilt in each walk from the (L1/L2-resident) trial cameras instead of being shuffled.
-// A landmark with k > 32 fills a slot alone and is processed by the whole warp.
+// A landmark with k > KSHORT fills a slot alone and is processed by the whole warp.
 __device__ __forceinline__ Rows4 resolve_obs(const Graph& g, const double* __restrict__ tcam,
                                              int o, const Coef& k) {
   const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
@@ -1808,7 +1817,7 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
   const int kk = e.z;                                     // warp-uniform
   double cost = 0.0;
   int rankdef = 0, fallback = 0;
-  if (kk > 32) {  // one long landmark: the warp strides over its observations
+  if (kk > KSHORT) {  // one long landmark: the warp strides over its observations
     const int l = __shfl_sync(PV_FULL, e.x, 0), o0 = __shfl_sync(PV_FULL, e.y, 0);
     const int oend = o0 + kk;
     double g1[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};

@@ -141,7 +141,7 @@ __device__ PV_SER_FN void series_reduce_list(const SeriesArgs& a, int r0, int r1
       const int kp = 32 * w + lane;
       const int s0 = __shfl_sync(PV_FULL, e.w, 0);  // lane 0's entry = the slot's base
       char* base = reinterpret_cast<char*>(a.sbuf) + 32 * (size_t)s0;
-      if (k > 32) {  // one long landmark: the whole warp, coalesced, fixed-order tree (lr_long)
+      if (k > KSHORT) {  // one long landmark: the whole warp, coalesced, fixed-order tree (lr_long)
         const int l0 = __shfl_sync(PV_FULL, e.x, 0);
         if (STAGE == 2 && lane == 0) pre.x = ldg4_h(a.lrec + (size_t)l0 * LREC);
         double a2[NV];
