@@ -272,3 +272,40 @@ def test_graph_term_loop_matches_host_loop(pv, max_order, thr):
     np.testing.assert_array_equal(a.landmark_update, b.landmark_update)
     if thr == 0.0:
         assert a.power_order_used == max_order
+
+
+@pytest.mark.parametrize("block_kb", [1 << 20, 176, 120])
+def test_few_blocks_many_cameras_all_term_paths(pv, block_kb):
+    """600 cameras x 2,500 landmarks (about 16 observations per camera): one warp per camera
+    even with a single landmark block, so the pipelined kernel, the term graph and the
+    one-kernel series all run with B = 1, 2 and 3 blocks (the series' first and last steps
+    drop their out-of-range parts) -- each must reproduce k_cam bit for bit, stage 1 and 2,
+    with tracks longer than a warp slot present (power-law lengths up to 150)."""
+    from paper_2405_05079_b200 import _lib, synth
+    cfg = synth.SynthConfig("wide", 600, 2500, ("power", 4.0, 150))
+    problem, _ = synth.make_problem(cfg, 3)
+    st1 = synth.random_state(problem, 2)
+    for stage in (1, 2):
+        st = st1 if stage == 1 else pv.lift_stage1_to_stage2(st1)
+        outs, blocks = [], None
+        for knobs in ([(_lib.PV_OPT_CAM_PIPE, 0)], [(_lib.PV_OPT_CAM_PIPE, 1)],
+                      [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_GRAPH, 0)],
+                      [(_lib.PV_OPT_CAM_PIPE, 1), (_lib.PV_OPT_SERIES, 1)]):
+            dp = pv.DeviceProblem(problem, 0.1)
+            dp.set_option(_lib.PV_OPT_BLOCK_BYTES, block_kb << 10)
+            for k, v in knobs:
+                dp.set_option(k, v)
+            info = dp.info()
+            assert info["warps_per_cam"] == 1
+            blocks = info["blocks"]
+            dp.set_state(st)
+            dp.linearize(stage)
+            dp.damp(1e-4, stage == 2)
+            order, trunc = dp.power_solve(6, 0.0)
+            dx, dl = dp.step(stage)
+            outs.append((order, trunc, dx.copy(), dl.copy()))
+        assert blocks == {1 << 20: 1, 176: 2, 120: 3}[block_kb], blocks
+        for o in outs[1:]:
+            assert o[0] == outs[0][0] == 6 and o[1] == outs[0][1]
+            np.testing.assert_array_equal(o[2], outs[0][2])
+            np.testing.assert_array_equal(o[3], outs[0][3])
