@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <mutex>
@@ -319,35 +320,42 @@ static void build_graph(pv_ctx* c, const int64_t* cam_idx, const int64_t* lm_idx
   c->n_ls = n_ls;
   c->n_os = (int)n_os;
 
-  // stable counting sort by camera, then stable by local landmark
-  std::vector<int64_t> ccount(n_p + 1, 0);
-  for (int64_t o = 0; o < n_o; ++o) {
-    int64_t l = lm_idx[o];
-    if (l >= lm_begin && l < lm_end) ccount[cam_idx[o] + 1]++;
-  }
-  for (int64_t i = 0; i < n_p; ++i) ccount[i + 1] += ccount[i];
-  std::vector<int64_t> by_cam(n_os);
-  {
-    std::vector<int64_t> pos(ccount.begin(), ccount.end() - 1);
-    for (int64_t o = 0; o < n_o; ++o) {
-      int64_t l = lm_idx[o];
-      if (l >= lm_begin && l < lm_end) by_cam[pos[cam_idx[o]]++] = o;
-    }
-  }
+  // landmark-major order with the cameras of a landmark ascending (ties in input order): one
+  // counting sort by local landmark, then a stable insertion sort of each landmark's few
+  // observations by camera -- the same order as a stable sort by camera followed by a stable
+  // sort by landmark, with one random pass over the observations instead of two
   std::vector<int> lm_off(n_ls + 1, 0);
   for (int j = 0; j < n_ls; ++j) lm_off[j + 1] = lm_off[j] + (int)cnt[c->lm_gid[j] - lm_begin];
   std::vector<int> ls_cam(n_os), ls_lid(n_os);
   std::vector<double> ls_m(2 * n_os);
   {
+    std::vector<int64_t> src(n_os);  // input index of every landmark-sorted slot
     std::vector<int> pos(lm_off.begin(), lm_off.end() - 1);
-    for (int64_t k = 0; k < n_os; ++k) {
-      int64_t o = by_cam[k];
-      int l = lid[lm_idx[o] - lm_begin];
-      int p = pos[l]++;
-      ls_cam[p] = (int)cam_idx[o];
-      ls_lid[p] = l;
-      ls_m[2 * p] = meas[2 * o];
-      ls_m[2 * p + 1] = meas[2 * o + 1];
+    for (int64_t o = 0; o < n_o; ++o) {
+      const int64_t l = lm_idx[o];
+      if (l >= lm_begin && l < lm_end) src[pos[lid[l - lm_begin]]++] = o;
+    }
+    for (int j = 0; j < n_ls; ++j) {
+      int64_t* a = src.data() + lm_off[j];
+      const int k = lm_off[j + 1] - lm_off[j];
+      for (int i = 1; i < k; ++i) {  // stable: equal cameras keep their input order
+        const int64_t v = a[i];
+        const int64_t cv = cam_idx[v];
+        int q = i - 1;
+        while (q >= 0 && cam_idx[a[q]] > cv) {
+          a[q + 1] = a[q];
+          --q;
+        }
+        a[q + 1] = v;
+      }
+      for (int i = 0; i < k; ++i) {
+        const int64_t o = a[i];
+        const int p = lm_off[j] + i;
+        ls_cam[p] = (int)cam_idx[o];
+        ls_lid[p] = j;
+        ls_m[2 * p] = meas[2 * o];
+        ls_m[2 * p + 1] = meas[2 * o + 1];
+      }
     }
   }
   // landmark tasks: whole landmarks packed into <= 32 lanes, or one long landmark;
@@ -816,6 +824,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
 }
 
 static void build_blocks(pv_ctx* c) {
+  const auto tbb = std::chrono::steady_clock::now();
   const int n_os = c->n_os, n_tasks = c->n_tasks;
   const int64_t n_p = c->n_p;
   const int64_t want = std::max<int64_t>(1, ((int64_t)n_os * 32 + c->block_bytes - 1) /
@@ -882,8 +891,15 @@ static void build_blocks(pv_ctx* c) {
   c->g.n_blk = B;
   c->g.seg = c->d_seg;
   c->lin_stage = 0;  // camera-sorted copies of x must be rebuilt
+  const auto tb0 = std::chrono::steady_clock::now();
   build_ktasks(c, cs_pos, cs_lm);  // replaces d_cs_pos (landmark-sorted positions) by s positions
+  const auto tb1 = std::chrono::steady_clock::now();
   build_pipe_items(c, seg);
+  if (std::getenv("PV_DEBUG_SETUP"))
+    std::fprintf(stderr, "build_blocks: sort+upload %.0f ms, ktasks %.0f ms, pipe items %.0f ms\n",
+                 std::chrono::duration<double, std::milli>(tb0 - tbb).count(),
+                 std::chrono::duration<double, std::milli>(tb1 - tb0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb1).count());
   c->h_seg = seg;
   if (c->cpart) ensure_cpart(c);   // re-blocking changes the number of warp slots
 }
@@ -1637,10 +1653,21 @@ int pv_create(pv_ctx** out, int device, int rank, int world, const unsigned char
         NK(ncclCommInitRank(&c->comm, world, id, rank));
       }
     }
+    const bool dbg = std::getenv("PV_DEBUG_SETUP") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t0 = now();
     build_graph(c, cam_idx, lm_idx, meas, lm_begin, lm_end);
+    const auto t1 = now();
     build_blocks(c);
+    const auto t2 = now();
     alloc_buffers(c);
     c->sync();
+    if (dbg)
+      std::fprintf(stderr, "pv_create: build_graph %.0f ms, build_blocks %.0f ms, alloc %.0f ms\n",
+                   ms(t0, t1), ms(t1, t2), ms(t2, now()));
   } catch (const std::exception& e) {
     g_create_error = e.what();
     int code = PV_ECUDA;
