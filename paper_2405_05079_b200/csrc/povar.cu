@@ -1025,7 +1025,7 @@ static void op_damp(pv_ctx* c, double lam, int both, int64_t* n_deg) {
   c->damp_lin_id = -1;
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_U, 0, 2 * sizeof(int), c->stream));
   CK(cudaMemsetAsync(c->flags + F_SINGULAR_M2, 0, sizeof(int), c->stream));
-  k_damp_cam<<<blocks_for(c->n_p, 64), 64, 0, c->stream>>>((int)c->n_p, D, c->cU, lam, c->cUd,
+  k_damp_cam<<<blocks_for(c->n_p * 32, 128), 128, 0, c->stream>>>((int)c->n_p, D, c->cU, lam, c->cUd,
                                                            c->cUi, c->flags);
   c->launched();
   if (both || !c->vp_cached) {
@@ -1423,7 +1423,7 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   c->check_launch();
   c->allreduce(c->cmom, np * 60);
   k_diag_finish<S><<<wg, 256, 0, c->stream>>>((int)np, c->cmom, c->ch, c->cUd, c->csd);
-  k_damp_cam<<<blocks_for(np, 64), 64, 0, c->stream>>>((int)np, D, c->csd, 0.0, c->csdd, c->cmi,
+  k_damp_cam<<<blocks_for(np * 32, 128), 128, 0, c->stream>>>((int)np, D, c->csd, 0.0, c->csdd, c->cmi,
                                                        c->flags + (F_SINGULAR_M - F_SINGULAR_U));
   c->launched(2);
   c->check_launch();
