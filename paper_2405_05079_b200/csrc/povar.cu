@@ -460,12 +460,15 @@ static void ensure_cpart(pv_ctx* c) {
   c->cpart_cap = need;
 }
 
-// Work lists of k_cam_pipe (pv_pipe.cuh).  Every (camera, block) segment is cut into items of
-// <= PCH observations; per landmark block there are three families of per-warp lists:
+// Work lists of k_cam_pipe (pv_pipe.cuh) and k_series (pv_series.cuh).  Every (camera, block)
+// segment is cut into items of <= PCH observations; per landmark block there are four
+// families of per-warp lists, plus the per-warp landmark-reduce slot lists of k_series:
 //   0: W t items (>= 1 per camera so that y is always written).  A camera's items stay with
 //      one warp (it owns the camera's sum);
 //   1: W^T v items for a pass launched on its own;
-//   2: W^T v items of block b for the launch that also runs the W t items of block b - 1.
+//   2: W^T v items of block b for the launch that also runs the W t items of block b - 1;
+//   3: W^T v items of block b for the k_series step that also runs the reduce slots of block
+//      b - 1 and the W t items of block b - 2.
 // Balance (bal_mode 1): the cost of an item is n + bal_item + bal_round * ceil(n / 32)
 // (+ bal_last on a camera's last W t item), in observation-equivalents.  Family 0 packs
 // whole cameras longest-first onto the least loaded warp; W^T v items are independent, so
