@@ -75,6 +75,8 @@ enum {
   /* bytes of x and m streamed per observation by a stage-1 camera pass (48, or 40 with the
    * compact stream of PV_OPT_XM) */
   PV_INFO_XM_BYTES = 18,
+  /* warps of the persistent camera kernel (resident CTAs per SM x SMs x warps per CTA) */
+  PV_INFO_PIPE_WARPS = 19,
   PV_INFO_COUNT = 24
 };
 

@@ -23,7 +23,7 @@ PV_CURRENT, PV_TRIAL = 0, 1
 INFO_FIELDS = ("n_p", "n_l_local", "n_o_local", "tasks", "chunks", "launches", "rank", "world",
                "device_bytes", "n_l_global", "resolve_fallbacks", "blocks", "persist_l2",
                "warps_per_cam", "solve_rhs_us", "solve_terms_us", "solve_backsub_us",
-               "solve_terms_launched", "xm_bytes")
+               "solve_terms_launched", "xm_bytes", "pipe_warps")
 PV_INFO_COUNT = 24
 (PV_OPT_STAGE_CAP, PV_OPT_POL_STREAM, PV_OPT_POL_T, PV_OPT_POL_S, PV_OPT_DISCARD_S,
  PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, _PV_OPT_RESERVED7, PV_OPT_CAM_PIPE,

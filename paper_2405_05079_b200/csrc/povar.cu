@@ -1729,6 +1729,7 @@ int pv_info(pv_ctx* c, int64_t* out) {
   out[PV_INFO_SOLVE_TERMS_US] = c->solve_us[1];
   out[PV_INFO_SOLVE_BACKSUB_US] = c->solve_us[2];
   out[PV_INFO_SOLVE_TERMS_LAUNCHED] = c->solve_terms_launched;
+  out[PV_INFO_PIPE_WARPS] = c->pipe_W;
   out[PV_INFO_XM_BYTES] = (c->xm_ok && c->tune.xm && c->tune.cam_pipe && c->wpc == 1) ? 40 : 48;
   API_END(c)
 }

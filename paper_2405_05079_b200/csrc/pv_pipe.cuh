@@ -31,14 +31,18 @@ namespace pv {
 #ifndef PV_PIPE_D
 #define PV_PIPE_D 3
 #endif
-// Shape (vlarge LM iteration, tools/lm_iter_time.py; profiles/r1_history.md): 3 warps per
-// CTA, 5 CTAs per SM (15 resident warps, 120 registers) 18.24 ms; 2 x 8 (14 warps, the
-// shared-memory limit) 18.29; ring depth 2 19.06; depth 4 (12 warps) 18.57.
+// Shape.  Round 1 (t gathered through shared memory): 3 warps x 5 CTAs per SM (15 resident
+// warps, 120 registers) 18.24 ms per LM iteration; 2 x 8 18.29; ring depth 2 19.06; depth 4
+// (12 warps) 18.57.  Round 2, with t in registers (PV_PIPE_TREG) the ring is 10.4 KB per warp
+// and the registers (120-124) are the only limit: term 1.051 ms (shared-memory t, 3 x 5) ->
+// 1.022 (3 x 5) -> 1.010 (4 x 4) / 1.012 (2 x 8) -> 0.980 ms with ONE warp per CTA (17 resident
+// CTAs per SM); register caps of 112 / 104 / 96 (18-21 warps) spill into the item loop and
+// lose (1.13 / 1.36 / 1.48 ms); depth 4 no gain (profiles/r2_series.md section 6).
 #ifndef PV_PIPE_W
-#define PV_PIPE_W 3
+#define PV_PIPE_W 1
 #endif
 #ifndef PV_PIPE_MINB
-#define PV_PIPE_MINB 5
+#define PV_PIPE_MINB 16
 #endif
 // The slot refilled at iteration c was consumed at iteration c-1, whose shared-memory
 // reads all fed instructions that have retired (and a __syncwarp) before the TMA is
@@ -57,7 +61,13 @@ constexpr int PI_BYTES = (PCH + 4) * 4;
 constexpr int PC_OFF = PI_OFF + PI_BYTES;  // camera record: P (12) | v (12)
 constexpr int PH_OFF = PC_OFF + 192;       // header {cam, o, n, flags}
 constexpr int PSLOT = ((PH_OFF + 16 + 31) / 32) * 32;
-constexpr int PT_BYTES = PCH * 32;          // gathered t of one chunk
+// PV_PIPE_TREG = 1: the t_j of the next W t item are loaded straight into registers by 256-bit
+// loads (one L1TEX request per observation) instead of two 16-byte cp.async per observation
+// into a shared-memory double buffer; the 4 KB per warp this frees can hold a deeper ring.
+#ifndef PV_PIPE_TREG
+#define PV_PIPE_TREG 1
+#endif
+constexpr int PT_BYTES = PV_PIPE_TREG ? 0 : PCH * 32;  // gathered t of one chunk
 constexpr int PWARP = PD * PSLOT + 2 * PT_BYTES;
 constexpr int PBAR = ((PW * PD * 8 + 127) / 128) * 128;
 constexpr int PIPE_SMEM = PBAR + PW * PWARP;
@@ -128,7 +138,11 @@ struct PipeItems {
 // cs_m1 holds m1 -- 40 instead of 48 bytes of x and m per observation (k_build_csx); x.w = 1
 // and m are rebuilt in registers, so both layouts give the same bits.
 template <int STAGE, bool HC, bool HA, bool XM>
+#ifdef PV_PIPE_MAXNREG
+__global__ void __maxnreg__(PV_PIPE_MAXNREG) k_cam_pipe(Graph g, PipeItems it,
+#else
 __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, PipeItems it,
+#endif
                                                       const double* __restrict__ crec,
                                                       const double* __restrict__ cs_x,
                                                       const double* __restrict__ cs_m1,
@@ -220,11 +234,23 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
     ++n_prod;
   };
   // t_j of every observation of a W t item (its ids have landed)
+  double4 Tn[(PCH + 31) / 32];  // PV_PIPE_TREG: t_j of the next W t item
   auto gather = [&](int item) {
     const unsigned char* slot = wsm + (item % PD) * PSLOT;
     const int4 h = *reinterpret_cast<const int4*>(slot + PH_OFF);
     if (h.w & PF_HA) return;
     const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (h.y & 3);
+#if PV_PIPE_TREG
+#pragma unroll
+    for (int r = 0; r < (PCH + 31) / 32; ++r) {
+      const int q = lane + 32 * r;
+      if (q < h.z) {
+        PV_CHECK(si[q] >= 0 && si[q] < g.n_kent);
+        Tn[r] = ld4cg(tarr + 4 * (size_t)si[q], pt);
+      }
+    }
+    return;
+#endif
     unsigned char* tb = tbuf + (item & 1) * PT_BYTES;
 #pragma unroll
     for (int r = 0; r < (PCH + 31) / 32; ++r) {
@@ -251,6 +277,11 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
 
   for (int c = 0; c < total; ++c) {
     produce();  // refills the slot consumed in the previous iteration
+#if PV_PIPE_TREG
+    double4 Tc[(PCH + 31) / 32];  // this item's t_j, loaded during the previous item
+#pragma unroll
+    for (int r = 0; r < (PCH + 31) / 32; ++r) Tc[r] = Tn[r];
+#endif
     if (c + 1 < total) {  // t gathers of the next item, in flight while this one computes
       mbar_wait(bars + (c + 1) % PD, (unsigned)(((c + 1) / PD) & 1));
       __syncwarp();
@@ -289,7 +320,11 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_cam_pipe(Graph g, Pip
             double4 X;
             double2 m;
             xm_at(q, X, m);
+            #if PV_PIPE_TREG
+            const double4 T = Tc[r];
+#else
             const double4 T = tq[q];
+#endif
             const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
             double sg[3];
             proj_map<STAGE>(pj, dot4(P0, T), dot4(P1, T), dot4(P2v, T), sg[0], sg[1], sg[2]);

@@ -256,8 +256,12 @@ __device__ int g_ser_term = 2, g_ser_step = 5;
   } while (0)
 #endif
 template <int STAGE, bool XM>
+#ifdef PV_PIPE_MAXNREG
+__global__ void __maxnreg__(PV_PIPE_MAXNREG) k_series(Graph g, SeriesArgs a, Coef k, Tune tune) {
+#else
 __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, SeriesArgs a, Coef k,
                                                                   Tune tune) {
+#endif
   extern __shared__ __align__(128) unsigned char pipe_dsm[];
   __shared__ int s_last;
   __shared__ double s_rr[2][8];
@@ -364,11 +368,23 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
         }
         ++n_prod;
       };
+      double4 Tn[(PCH + 31) / 32];  // PV_PIPE_TREG: t_j of the next W t item
       auto gather = [&](int item) {  // item: index within this step
         const unsigned char* slot = wsm + ((gbase + item) % PD) * PSLOT;
         const int4 h = *reinterpret_cast<const int4*>(slot + PH_OFF);
         if (h.w & PF_HA) return;
         const int* si = reinterpret_cast<const int*>(slot + PI_OFF) + (h.y & 3);
+#if PV_PIPE_TREG
+#pragma unroll
+        for (int r = 0; r < (PCH + 31) / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (q < h.z) {
+            PV_CHECK(si[q] >= 0 && si[q] < g.n_kent);
+            Tn[r] = ld4cg(a.tarr + 4 * (size_t)si[q], pt);
+          }
+        }
+        return;
+#endif
         unsigned char* tb = tbuf + (item & 1) * PT_BYTES;
 #pragma unroll
         for (int r = 0; r < (PCH + 31) / 32; ++r) {
@@ -395,6 +411,11 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
 
       for (int c = 0; c < total; ++c) {
         produce();
+#if PV_PIPE_TREG
+        double4 Tc[(PCH + 31) / 32];  // this item's t_j, loaded during the previous item
+#pragma unroll
+        for (int r = 0; r < (PCH + 31) / 32; ++r) Tc[r] = Tn[r];
+#endif
         if (c + 1 < total) {
           const int gi = gbase + c + 1;
           mbar_wait(bars + gi % PD, (unsigned)((gi / PD) & 1));
@@ -432,7 +453,11 @@ __global__ void __launch_bounds__(PW * 32, PV_PIPE_MINB) k_series(Graph g, Serie
               double4 X;
               double2 m;
               xm_at(q, X, m);
-              const double4 T = tq[q];
+              #if PV_PIPE_TREG
+            const double4 T = Tc[r];
+#else
+            const double4 T = tq[q];
+#endif
               const Proj pj = STAGE == 1 ? proj_s1(m.x, m.y, k.s) : proj_s2(P0, P1, P2v, X);
               double sg[3];
               proj_map<STAGE>(pj, dot4(P0, T), dot4(P1, T), dot4(P2v, T), sg[0], sg[1], sg[2]);

@@ -35,7 +35,7 @@ B = dp.info()["blocks"]
 n_items = ctypes.c_int(0)
 fn(dp._ctx, ctypes.c_int(blk), None, ctypes.byref(n_items), None, ctypes.c_int(0), None)
 dp.bench_terms(1, 3)
-W = 148 * 5 * 3
+W = dp.info()["pipe_warps"]
 # find W from the offsets: 3 * B * (W + 1) ints
 items = np.zeros((n_items.value, 4), np.int32)
 for Wt in (W, 148 * 4 * 3, 148 * 6 * 3, 148 * 3 * 3):

@@ -31,7 +31,7 @@ for kv in sys.argv[4:]:
 fn = dp._lib.pv_debug_series_times
 fn.restype = ctypes.c_int
 B = dp.info()["blocks"]
-W = 148 * 5 * 3
+W = dp.info()["pipe_warps"]
 fn(dp._ctx, ctypes.c_int(2), ctypes.c_int(step), None, None, None, None)
 dp.bench_terms(stage, 3)
 r = dp.bench_terms(stage, 10)
