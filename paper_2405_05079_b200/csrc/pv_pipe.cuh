@@ -13,8 +13,9 @@
 //   * streams (x, m, ids of a chunk + the 192-byte camera record) are fetched by
 //     TMA bulk copies (cp.async.bulk, one elected lane, mbarrier completion)
 //     D-1 chunks ahead, across camera and phase boundaries;
-//   * the t gathers of chunk c+1 (cp.async, 2 x 16 B per observation, L2) are
-//     issued before chunk c is computed;
+//   * the t_j of chunk c+1 (L2) are loaded before chunk c is computed, by one 256-bit load
+//     per observation straight into registers (PV_PIPE_TREG; round 1: two 16-byte cp.async
+//     per observation into a shared-memory double buffer);
 //   * the work list itself (item descriptors, built on the host) is read 32 items
 //     at a time, one window ahead.
 //
