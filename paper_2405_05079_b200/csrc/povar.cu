@@ -188,6 +188,9 @@ struct pv_ctx {
   int layout_gen = 0;  // bumped whenever device work lists are rebuilt (term-graph cache key)
   int lr_ctas_per_sm = 3;  // lvr/lbl hold the stage-1 landmark linearization of the current state
   double *d_ls_m = nullptr, *d_cs_m = nullptr;
+  double* d_ks_m = nullptr;  // slot-interleaved copies of ls_m / ls_cam (s positions)
+  int* d_ks_cam = nullptr;
+  size_t ks_entries = 0;
 
   // state and solve buffers (device)
   double *crec, *lrec, *lvr, *lbl, *ldl, *tlm, *tcam, *cs_x, *cs_xm;
@@ -784,6 +787,26 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
     free_tracked(c, c->sbuf, c->sbuf_doubles * sizeof(double));
     c->sbuf = c->alloc<double>(need);
     c->sbuf_doubles = need;
+  }
+  {  // slot-interleaved copies of the landmark-sorted measurements and camera ids
+    const size_t ne = std::max<size_t>((size_t)sn, 1);
+    free_tracked(c, c->d_ks_m, c->ks_entries * 2 * sizeof(double));
+    free_tracked(c, c->d_ks_cam, c->ks_entries * sizeof(int));
+    c->d_ks_m = c->alloc<double>(ne * 2);
+    c->d_ks_cam = c->alloc<int>(ne);
+    c->ks_entries = ne;
+    int* d_spos = nullptr;
+    CK(cudaMalloc(&d_spos, std::max<size_t>((size_t)c->n_os, 1) * sizeof(int)));
+    CK(cudaMemcpyAsync(d_spos, spos.data(), (size_t)c->n_os * sizeof(int), cudaMemcpyHostToDevice,
+                       c->stream));
+    k_scatter_ks<<<blocks_for(c->n_os, 256), 256, 0, c->stream>>>(c->n_os, d_spos, c->d_ls_m,
+                                                                 c->d_ls_cam, c->d_ks_m,
+                                                                 c->d_ks_cam);
+    c->launched();
+    c->sync();
+    CK(cudaFree(d_spos));
+    c->g.ks_m = c->d_ks_m;
+    c->g.ks_cam = c->d_ks_cam;
   }
   // s position of every camera-sorted observation (the scatter target of W^T v) and the
   // slot position of its landmark (the gather index of t and V+)

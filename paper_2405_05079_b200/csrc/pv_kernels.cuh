@@ -74,6 +74,12 @@ struct Graph {
   const int* seg;        // [n_blk*n_p+1] start of segment (block b, camera c) at b*n_p+c in the
                          // block-major camera-sorted order (block, camera, landmark)
   const double* cs_m;    // [n_o*2]
+  // measurements and cameras of the landmark-sorted observations once more, at their s
+  // position (the warp-slot interleaved layout of build_ktasks): the lane-per-landmark walks
+  // of the re-solve and the landmark linearization read 32 lanes' observation i with one
+  // coalesced request instead of 32 scattered ones
+  const double* ks_m;    // [n_s*2]
+  const int* ks_cam;     // [n_s]
 };
 
 // stop / report state of the inner solve, shared by the power series and PCG
@@ -783,6 +789,18 @@ __global__ void k_build_csx(Graph g, const double* __restrict__ lrec, double* __
   }
 }
 
+// slot-interleaved copies of the landmark-sorted measurements and camera ids (once per
+// re-blocking): entry spos[p] <- landmark-sorted observation p
+__global__ void k_scatter_ks(int n_o, const int* __restrict__ spos, const double* __restrict__ ls_m,
+                             const int* __restrict__ ls_cam, double* __restrict__ ks_m,
+                             int* __restrict__ ks_cam) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_o) return;
+  const int q = __ldg(spos + p);
+  reinterpret_cast<double2*>(ks_m)[q] = reinterpret_cast<const double2*>(ls_m)[p];
+  ks_cam[q] = __ldg(ls_cam + p);
+}
+
 // m1 of every block-major camera-sorted observation (once per re-blocking)
 __global__ void k_gather_m1(int n_o, const double* __restrict__ cs_m, double* __restrict__ cs_m1) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -902,9 +920,10 @@ __global__ void __launch_bounds__(256) k_lin_lm_slots(Graph g, const int4* __res
     const double xv[4] = {x.x, x.y, x.z, x.w};
     householder_h<4>(xv, h);
   }
-  for (int o = e.y; o < e.y + kk; ++o) {
-    const double2 m = ldg2(g.ls_m + 2 * (size_t)o);
-    lin_lm_obs<STAGE>(crec, __ldg(g.ls_cam + o), m.x, m.y, x, h, k, acc, flags);
+  for (int i = 0; i < kk; ++i) {  // observation i of this lane's landmark at s position e.w + 32 i
+    const int pos = e.w + 32 * i;
+    const double2 m = ldg2(g.ks_m + 2 * (size_t)pos);
+    lin_lm_obs<STAGE>(crec, __ldg(g.ks_cam + pos), m.x, m.y, x, h, k, acc, flags);
   }
   lin_lm_finish(e.x, acc, lvr, lbl);
 }
@@ -1785,6 +1804,13 @@ __device__ __forceinline__ Rows4 resolve_obs(const Graph& g, const double* __res
   return resolve_rows4(tcam, __ldg(g.ls_cam + o), m.x, m.y, k);
 }
 
+// the same observation by its s position (lane-per-landmark walks: coalesced across the slot)
+__device__ __forceinline__ Rows4 resolve_obs_s(const Graph& g, const double* __restrict__ tcam,
+                                               int pos, const Coef& k) {
+  const double2 m = ldg2(g.ks_m + 2 * (size_t)pos);
+  return resolve_rows4(tcam, __ldg(g.ks_cam + pos), m.x, m.y, k);
+}
+
 // per-landmark solve from the pass-1 Gram (returns fb: 0 solved, 1 needs pass 2, 2 Givens)
 __device__ __forceinline__ int resolve_pass1(const double* g1, double* R1, double* v) {
   const double ratio = chol3(g1, R1);
@@ -1870,11 +1896,13 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
     for (int o = o0 + lane; o < oend; o += 32) cost += rows_cost(resolve_obs(g, tcam, o, k), x);
   } else {
     const bool act = e.x >= 0;
-    const int l = e.x, o0 = e.y, oend = act ? e.y + kk : e.y;
+    const int l = e.x, o0 = e.y;
+    // observation i of this lane's landmark sits at s position e.w + 32 i (ks_m / ks_cam)
+    const int p0 = e.w, pend = act ? e.w + 32 * kk : e.w;
     double g1[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     double cc = 0.0;  // c^T c, for the cost at the solution from the Gram (below)
-    for (int o = o0; o < oend; ++o) {
-      const Rows4 rw = resolve_obs(g, tcam, o, k);
+    for (int pos = p0; pos < pend; pos += 32) {
+      const Rows4 rw = resolve_obs_s(g, tcam, pos, k);
       gram6(rw, g1);
 #pragma unroll
       for (int r = 0; r < 4; ++r) cc = fma(rw.c[r], rw.c[r], cc);
@@ -1885,13 +1913,13 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
     if (fb == 1) {
       const double id[3] = {1.0 / R1[0], 1.0 / R1[3], 1.0 / R1[5]};
       double s2[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      for (int o = o0; o < oend; ++o) gram_pass2(resolve_obs(g, tcam, o, k), R1, id, s2);
+      for (int pos = p0; pos < pend; pos += 32) gram_pass2(resolve_obs_s(g, tcam, pos, k), R1, id, s2);
       full = cqr2_solve(R1, s2, v);
     } else if (fb == 2) {
       fallback = 1;
       double Rg[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-      for (int o = o0; o < oend; ++o) {
-        const Rows4 rw = resolve_obs(g, tcam, o, k);
+      for (int pos = p0; pos < pend; pos += 32) {
+        const Rows4 rw = resolve_obs_s(g, tcam, pos, k);
         for (int r = 0; r < 4; ++r) givens_row(Rg, rw.a[r][0], rw.a[r][1], rw.a[r][2], rw.c[r]);
       }
       full = lsq_from_r(Rg, 1e-10, v);
@@ -1924,7 +1952,8 @@ __global__ void __launch_bounds__(256) k_resolve_slots(Graph g, const int4* __re
       xu.y = __shfl_sync(PV_FULL, x.y, u);
       xu.z = __shfl_sync(PV_FULL, x.z, u);
       xu.w = __shfl_sync(PV_FULL, x.w, u);
-      const double cu = lane < kk ? rows_cost(resolve_obs(g, tcam, uo + lane, k), xu) : 0.0;
+      double cu = 0.0;  // kk <= KSHORT observations: lane q takes q, q + 32, ...
+      for (int q = lane; q < kk; q += 32) cu += rows_cost(resolve_obs(g, tcam, uo + q, k), xu);
       const double su = warp_sum(cu);
       if (lane == u) cost = su;
     }

@@ -190,3 +190,40 @@ def test_collective_code_path_matches_fused(pv, stage):
     # and the multi-block trace agrees with the oracle
     log = O.lm_minimize(O.graph_of(pr), st.cameras, st.landmarks, stage, max_iterations=6)
     np.testing.assert_allclose(runs[0][0], log.costs, rtol=1e-6, atol=0)
+
+
+def test_resolve_cost_walk_covers_whole_slot_tracks(pv):
+    """Near-consistent affine data: after the re-solve a landmark's cost is ~1e-14 of the
+    terms of its Gram form, so k_resolve_slots walks the observations again for the cost
+    (the warp-cooperative path).  With lane-per-landmark slots up to KSHORT = 64
+    observations that walk must cover tracks longer than one warp: the cost returned by the
+    accept + re-solve equals the cost kernel's on the accepted state (track lengths on both
+    sides of 32 and of 64)."""
+    rng = np.random.default_rng(5)
+    n_c, n_l = 100, 36
+    ks = [20, 33, 40, 64, 65, 90]
+    ci, li = [], []
+    for j in range(n_l):
+        for c in sorted(rng.choice(n_c, size=ks[j % len(ks)], replace=False)):
+            ci.append(c)
+            li.append(j)
+    ci, li = np.array(ci), np.array(li)
+    cams = rng.standard_normal((n_c, 3, 4))
+    cams[:, 2, :] = 0.0
+    cams[:, 2, 3] = 1.0
+    lms = np.concatenate([rng.standard_normal((n_l, 3)), np.ones((n_l, 1))], axis=1)
+    meas = np.einsum("nij,nj->ni", cams[ci][:, :2, :], lms[li]) + 1e-7 * rng.standard_normal((len(ci), 2))
+    pr = _kat.problem(n_c, n_l, ci, li, meas)
+    start = np.array(lms)
+    start[:, :3] += 0.3 * rng.standard_normal((n_l, 3))
+    dp = pv.DeviceProblem(pr, 0.1)
+    dp.set_state(pv.ProjectiveState(cams, start))
+    f0 = dp.cost(1)
+    dp.linearize(1)
+    dp.damp(1e-4, False)
+    dp.power_solve(20, 0.01)
+    assert dp.trial(1)
+    f_new, _ = dp.accept(1, resolve=True)
+    f_chk = dp.cost(1)
+    assert f_new < 1e-8 * f0  # the re-solve recovers the consistent landmarks
+    assert abs(f_new - f_chk) <= 1e-8 * f_chk, (f_new, f_chk)
