@@ -118,12 +118,15 @@ enum {
   PV_OPT_BAL_LAST = 19,        /* camera's last W t item (its warp reduction)                    */
   PV_OPT_BAL_RFIX = 20,        /* ... and of a landmark-reduce slot of the series kernel: fixed  */
   PV_OPT_BAL_ROBS8 = 21,       /* + (partials * value) / 8                                       */
-  PV_OPT_SERIES = 22           /* 1: the whole power series (every term's landmark reduces, camera
+  PV_OPT_SERIES = 22,          /* 1: the whole power series (every term's landmark reduces, camera
                                   passes, U^-1 epilogue and stop test) runs as ONE persistent
                                   cooperative kernel with grid barriers (pv_series.cuh), bit-
                                   identical to 0 (default): one launch per landmark block and
                                   pass inside the term graph.  Measured 4% slower per LM
                                   iteration at vlarge (profiles/r2_series.md), so opt-in        */
+  PV_OPT_KSLOT = 23            /* 1 (default): the stage-1 landmark reduce of a term reads one
+                                  16-byte record per warp slot (L2-resident) instead of the
+                                  512-byte per-lane entries (results unchanged)                 */
 };
 
 /* NCCL unique id (128 bytes) for a multi-rank world; rank 0 creates it and the

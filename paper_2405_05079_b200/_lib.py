@@ -29,7 +29,8 @@ PV_INFO_COUNT = 24
  PV_OPT_BLOCK_BYTES, PV_OPT_FORCE_COLLECTIVE, _PV_OPT_RESERVED7, PV_OPT_CAM_PIPE,
  PV_OPT_RESOLVE_SLOTS, PV_OPT_SPLIT_LAST, PV_OPT_RHS_REUSE, PV_OPT_COST_CS,
  PV_OPT_BENCH_SPLIT, PV_OPT_XM, PV_OPT_GRAPH, PV_OPT_BALANCE, PV_OPT_BAL_ITEM,
- PV_OPT_BAL_ROUND, PV_OPT_BAL_LAST, PV_OPT_BAL_RFIX, PV_OPT_BAL_ROBS8, PV_OPT_SERIES) = range(23)
+ PV_OPT_BAL_ROUND, PV_OPT_BAL_LAST, PV_OPT_BAL_RFIX, PV_OPT_BAL_ROBS8, PV_OPT_SERIES,
+ PV_OPT_KSLOT) = range(24)
 
 # (name, restype, argtypes) of every exported symbol declared in include/povar.h
 _P = ctypes.c_void_p

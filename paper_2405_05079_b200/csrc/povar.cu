@@ -149,6 +149,9 @@ struct pv_ctx {
   std::vector<int> blk_ktask;  // [n_blk+1] warp slots
   int4* d_klist = nullptr;
   size_t klist_bytes = 0;
+  int use_kslot = 1;        // PV_OPT_KSLOT
+  int4* d_kslot = nullptr;  // per slot {k, s position, landmarks, first landmark} (stage-1 terms)
+  size_t kslot_bytes = 0;
   // V+ (lsys) and t (tarr) live in warp-slot order: landmark l at slot position h_lpos[l]
   // (klist entry index), camera-sorted observation o's landmark at d_cs_kpos[o]
   std::vector<int> h_lpos;
@@ -727,6 +730,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
   c->blk_ktask.assign(B + 1, 0);
   c->blk_s.assign(B + 1, 0);
   c->h_slot_n.clear();
+  std::vector<int4> kslot;
   std::vector<std::vector<int>> bucket(KSHORT + 1);
   for (int b = 0; b < B; ++b) {
     const int t0 = c->blk_task[b], t1 = c->blk_task[b + 1];
@@ -751,6 +755,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
       kl.push_back(make_int4(l, off[l], k, (int)sn));
       for (int q = 1; q < 32; ++q) kl.push_back(make_int4(-1, 0, k, 0));
       for (int i = 0; i < k; ++i) spos[off[l] + i] = (int)(sn + i);
+      kslot.push_back(make_int4(k, (int)sn, 1, l));
       sn += (k + 3) & ~3;  // whole 128-byte lines per slot (dropped from L2 slot by slot)
       c->h_slot_n.push_back(k);
     }
@@ -768,6 +773,7 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
             kl.push_back(make_int4(-1, 0, k, 0));
           }
         }
+        kslot.push_back(make_int4(k, (int)sn, n, v[i]));
         sn += 32 * (int64_t)k;
         c->h_slot_n.push_back(32 * k);
       }
@@ -780,6 +786,11 @@ static void build_ktasks(pv_ctx* c, const std::vector<int>& cs_ls, const std::ve
   c->d_klist = c->alloc<int4>(kl.size());
   c->klist_bytes = std::max<size_t>(kl.size(), 1) * sizeof(int4);
   CK(cudaMemcpyAsync(c->d_klist, kl.data(), kl.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                     c->stream));
+  free_tracked(c, c->d_kslot, c->kslot_bytes);
+  c->d_kslot = c->alloc<int4>(std::max<size_t>(kslot.size(), 1));
+  c->kslot_bytes = std::max<size_t>(kslot.size(), 1) * sizeof(int4);
+  CK(cudaMemcpyAsync(c->d_kslot, kslot.data(), kslot.size() * sizeof(int4), cudaMemcpyHostToDevice,
                      c->stream));
   // the partials buffer holds every slot's entries (padding lanes included)
   const size_t need = std::max<size_t>((size_t)sn, 1) * 4;
@@ -1139,7 +1150,7 @@ template <int S, int MODE>
 static void launch_lm_reduce(pv_ctx* c, int b_lo, int b_hi, int check_stop) {
   const int k_lo = c->blk_ktask[b_lo], k_hi = c->blk_ktask[b_hi];
   const int nb = blocks_for((long long)(k_hi - k_lo) * 32, 256);  // one task per warp
-  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->d_klist, c->sbuf, c->lrec,
+  k_lm_reduce<S, MODE><<<nb, 256, 0, c->stream>>>(c->d_klist, c->use_kslot ? c->d_kslot : nullptr, c->sbuf, c->lrec,
                                                   c->tarr, c->lsys, c->lbl, c->ldl, c->tlm,
                                                   c->ctl, c->flags, c->tune, k_lo, k_hi,
                                                   check_stop);
@@ -1825,6 +1836,10 @@ int pv_set_option(pv_ctx* c, int key, int64_t value) {
       break;
     case PV_OPT_SERIES:
       c->tune.series = value ? 1 : 0;
+      break;
+    case PV_OPT_KSLOT:
+      c->use_kslot = value ? 1 : 0;
+      ++c->layout_gen;  // the term graph captured the kernel argument
       break;
     case PV_OPT_BLOCK_BYTES:
       if (value < 4096) throw PvError(PV_EINVAL, "block budget too small");

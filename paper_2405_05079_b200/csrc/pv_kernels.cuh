@@ -707,6 +707,7 @@ constexpr int kLrUnroll = PV_LR_UNROLL;
 
 template <int STAGE, int MODE>
 __global__ void __launch_bounds__(256, PV_LR_MINB) k_lm_reduce(const int4* __restrict__ klist,
+                                                   const int4* __restrict__ kslot,
                                                    const double* __restrict__ sbuf,
                                                    const double* __restrict__ lrec,
                                                    double* __restrict__ tarr,
@@ -722,8 +723,17 @@ __global__ void __launch_bounds__(256, PV_LR_MINB) k_lm_reduce(const int4* __res
   if (w >= k_hi) return;
   if (check_stop && ctl->stopped) return;
   const uint64_t pf = pol_sel(tune.pol_s), pt = pol_sel(tune.pol_t);
-  const int4 e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k}
-  const int k = e.z;                                      // warp-uniform
+  int4 e;
+  if (STAGE == 1 && MODE == LR_TERM && kslot != nullptr) {
+    // stage-1 terms need no landmark ids: the slot's {k, s position, landmarks} come from one
+    // 16-byte record that every lane reads (4 MB for all slots: it stays in L2 from term to
+    // term, while the 512-byte per-lane entries (128 MB) are a DRAM round trip per slot)
+    const int4 ks = __ldg(kslot + w);
+    e = make_int4(lane < ks.z ? 0 : -1, 0, ks.x, ks.x > KSHORT ? ks.y : ks.y + lane);
+  } else {
+    e = __ldg(klist + 32 * (size_t)w + lane);  // {landmark, first obs, k, s position}
+  }
+  const int k = e.z;  // warp-uniform
   if (k > KSHORT) {
     Task t;
     t.l0 = __shfl_sync(PV_FULL, e.x, 0);

@@ -1,7 +1,7 @@
 """Term time vs the work-list balance of the persistent camera kernel (PV_OPT_BALANCE and its
 cost model, PV_OPT_BAL_ITEM / _ROUND / _LAST) on a BASELINE config; also checks that every
 setting gives the same power-series bits.
-Usage: [PV_DEBUG_BALANCE=1] python tools/sweep_balance.py [config] ["mode:item:round:last,..."]"""
+Usage: [PV_DEBUG_BALANCE=1] python tools/sweep_balance.py [config] ["mode:item:round:last[:kslot],..."]"""
 import hashlib
 import os
 import sys
@@ -22,7 +22,10 @@ dp.set_state(synth.random_state(problem, 1))
 dp.linearize(1)
 dp.damp(1e-4, False)
 for cb in combos.split(","):
-    mode, item, rnd, last = (int(x) for x in cb.split(":"))
+    f = [int(x) for x in cb.split(":")]
+    mode, item, rnd, last = f[:4]
+    if len(f) > 4:  # optional fifth field: PV_OPT_KSLOT
+        dp.set_option(_lib.PV_OPT_KSLOT, f[4])
     dp.set_option(_lib.PV_OPT_BAL_ITEM, item)
     dp.set_option(_lib.PV_OPT_BAL_ROUND, rnd)
     dp.set_option(_lib.PV_OPT_BAL_LAST, last)
