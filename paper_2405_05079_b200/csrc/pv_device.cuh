@@ -217,6 +217,38 @@ __device__ __forceinline__ void warp_reduce_all(double (&v)[N]) {
   }
 }
 
+// Fixed-order strided sum of per-item partials written earlier in the launch by other CTAs:
+// thread t adds part[(t + k * blockDim.x) * NV + v] for k = 0, 1, ... in order.  UB loads of
+// each chain are in flight at once (one L2 round trip per UB items instead of one per item: a
+// last-CTA reduction over 13,682 cameras went from ~54 to 4 dependent round trips); the
+// additions keep the one-at-a-time order, so the bits do too.
+template <int NV, int UB = 16>
+__device__ __forceinline__ void strided_sum_ordered(const double* part, int n, double (&a)[NV]) {
+  const int T = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + (UB - 1) * T < n; i += UB * T) {
+    double v[UB][NV];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      if (NV == 2) {
+        const double2 w = __ldcg(reinterpret_cast<const double2*>(part) + (i + u * T));
+        v[u][0] = w.x;
+        v[u][NV - 1] = w.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[u][q] = __ldcg(part + (size_t)(i + u * T) * NV + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) a[q] += v[u][q];
+  }
+  for (; i < n; i += T)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) a[q] += __ldcg(part + (size_t)i * NV + q);
+}
+
 // Sum of 12 per-lane values over the warp, returned in lane i for component i (i < 12).
 // A transposed butterfly: at each level a lane keeps half of its (padded to 16) values and
 // adds its partner's copy of them, so every component sees exactly the additions of

@@ -248,6 +248,9 @@ struct CamArgs {
 #ifndef PV_CAM_MINB
 #define PV_CAM_MINB 1
 #endif
+#ifndef PV_EP_MIRROR_ALWAYS
+#define PV_EP_MIRROR_ALWAYS 0
+#endif
 template <int STAGE, bool HC, int EP, bool HA>
 __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
     Graph g, double* __restrict__ crec, const double* __restrict__ cs_x,
@@ -492,12 +495,8 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double a = 0.0, bsum = 0.0;
-  for (int i = tid; i < g.n_p; i += blockDim.x) {
-    a += __ldcg(nrm + 2 * (size_t)i);
-    bsum += __ldcg(nrm + 2 * (size_t)i + 1);
-  }
-  double ra[2] = {a, bsum};
+  double ra[2] = {0.0, 0.0};
+  strided_sum_ordered<2>(nrm, g.n_p, ra);
   warp_reduce_all(ra);
   __shared__ double rr[2][8];
   if ((tid & 31) == 0) {
@@ -537,10 +536,9 @@ __global__ void __launch_bounds__(256, PV_CAM_MINB) k_cam(
     c.tnorm = TN;
     *ctl = c;
     // the host's look-ahead loop reads `stopped`, then `term`: publish term first, so a rank
-    // never sees the stop without the term that took it (povar.cu op_power).  (Skipping the
-    // mirror inside the term graph and prefetching the norm loads: LM iteration 19.94 ->
-    // 20.05 ms in an A/B on one box; kept as is.)
-    {
+    // never sees the stop without the term that took it (povar.cu op_power).  Inside the term
+    // graph (ca.cond) the host reads the control block once, after the series: no mirror
+    if (PV_EP_MIRROR_ALWAYS || !ca.cond) {
       host_ctl->order = c.order;
       host_ctl->term = c.term;
       host_ctl->trunc = c.trunc;

@@ -51,9 +51,7 @@ __device__ __forceinline__ bool last_cta_sum(const double* part, int n, unsigned
   double a[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) a[v] = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-#pragma unroll
-    for (int v = 0; v < NV; ++v) a[v] += __ldcg(part + (size_t)i * NV + v);
+  strided_sum_ordered<NV>(part, n, a);
   warp_reduce_all(a);
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
