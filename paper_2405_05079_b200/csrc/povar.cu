@@ -1213,12 +1213,18 @@ template <int S>
 static void launch_term(pv_ctx* c, int i, double thr, unsigned long long cond = 0,
                         int max_order = 0) {
   const int B = c->n_blk;
+  // Launched ahead by the host loop, a term's kernels return at once when an earlier term
+  // took the stop (one load of the control block at the head of every kernel).  Inside the
+  // term graph the body only runs while the series continues, so that load -- an L2 round
+  // trip in front of each of the 2 B + 2 kernels -- is dropped; only the next term's first
+  // W^T v pass, which follows the stop decision inside the same body, keeps it.
+  const int cs = cond ? 0 : 1;
   for (int b = 0; b < B; ++b) {
-    launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
+    launch_lm_reduce<S, LR_TERM>(c, b, b + 1, cs);
     if (b + 1 < B)
-      launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, i, thr, 1));
+      launch_cam<S, true, EP_NONE, true>(c, cam_args(b, b + 1, b == 0, b + 1, b + 2, i, thr, cs));
     else
-      launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, i, thr, 1, cond, max_order);
+      launch_cam_last<S, EP_TERM>(c, b, b + 1, b == 0, i, thr, cs, cond, max_order);
   }
 }
 
