@@ -309,3 +309,29 @@ def test_few_blocks_many_cameras_all_term_paths(pv, block_kb):
             assert o[0] == outs[0][0] == 6 and o[1] == outs[0][1]
             np.testing.assert_array_equal(o[2], outs[0][2])
             np.testing.assert_array_equal(o[3], outs[0][3])
+
+
+@pytest.mark.parametrize("config", ["small", "large"])
+def test_slot_records_match_lane_entries(pv, config):
+    """PV_OPT_KSLOT: the stage-1 term reduce reading one 16-byte record per warp slot gives
+    the per-lane entries' series bit for bit, in the host loop and in the term graph (small:
+    20 track lengths per block, partly filled slots; large: tracks longer than a 64-observation
+    slot, reduced by a whole warp)."""
+    from paper_2405_05079_b200 import _lib, synth
+    problem, _ = synth.make_problem(config, 0)
+    dp = pv.DeviceProblem(problem, 0.1)
+    dp.set_option(_lib.PV_OPT_BLOCK_BYTES, (64 << 10) if config == "small" else (8 << 20))
+    dp.set_state(synth.random_state(problem, 1))
+    out = []
+    for kslot, graph in ((0, 0), (1, 0), (1, 1)):
+        dp.set_option(_lib.PV_OPT_KSLOT, kslot)
+        dp.set_option(_lib.PV_OPT_GRAPH, graph)
+        dp.linearize(1)
+        dp.damp(1e-4, False)
+        order, trunc = dp.power_solve(6, 0.0)
+        dx, dl = dp.step(1)
+        out.append((order, trunc, dx.copy(), dl.copy()))
+    for o in out[1:]:
+        assert out[0][0] == o[0] == 6 and out[0][1] == o[1]
+        np.testing.assert_array_equal(out[0][2], o[2])
+        np.testing.assert_array_equal(out[0][3], o[3])
