@@ -122,14 +122,15 @@ def term_bytes(n_p, n_l, n_o, stage=1, xm_bytes=48):
     The camera passes stream the camera-sorted x and m (``xm_bytes``: 32 + 16, or 40 with
     the compact stage-1 stream of PV_OPT_XM) and one int32 id (4) twice -- once for W t, once for W^T v -- plus per camera the 192-byte record
     per pass and y (96); the landmark reduces read each landmark's V+ record (64) and
-    its work-slot entry (16; stage 2 also x, 32).  ``l2``: the transposes that the
+    (stage 2) its work-slot entry (16) and x (32); the stage-1 reduce reads one 16-byte record
+    per 32-landmark slot instead (PV_OPT_KSLOT: L2-resident, not counted).  ``l2``: the transposes that the
     landmark blocking keeps in the persisting L2 by design -- the partials s (written
     and read, 32 per observation) and the vectors t (written per landmark, gathered per
     observation).  ``r1_term``: the reference's own layout (W stored, SURVEY section
     8(d)), for the north_star's roofline figure.
     """
     cam = 2 * (xm_bytes + 4) * n_o + (2 * 192 + 96) * n_p
-    lmr = (80 if stage == 1 else 112) * n_l
+    lmr = (64 if stage == 1 else 112) * n_l
     l2 = {"cam": 32 * n_o + 32 * n_o, "lm_reduce": 32 * n_o + 32 * n_l}
     r1 = (292 if stage == 1 else 268) * n_o + 52 * n_l + (1632 if stage == 1 else 1408) * n_p
     return {"dram": {"cam": cam, "lm_reduce": lmr}, "l2": l2, "r1_term": r1}
@@ -429,7 +430,12 @@ def main():
                 "note": "per power-series term, summed over the landmark-block launches: "
                         "achieved = DRAM-compulsory bytes of the layout / summed launch time "
                         "(CUDA events around every launch); traffic = ncu dram bytes"}
-    non_term_ms = ms_step - float(np.mean(orders)) * spmv["ms_per_term"]
+    # the series' own device time (events around the term graph inside pv_power_solve): the
+    # terms actually launched per solve (order + 1: the term that takes the stop is applied,
+    # solvers.py:140-149) and what one of them takes inside the graph
+    tl = breakdown["terms_launched_per_step"]
+    ms_term_series = breakdown["solve_terms"] / tl if tl else None
+    non_term_ms = ms_step - breakdown["solve_terms"]
 
     # ---- PCG inner solver ("iterative", solvers.py:153-187) on the same system -----
     pcg = None
@@ -566,7 +572,8 @@ def main():
                            "parallelism": f"landmark-sharded dp{world}"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "ms_per_term": spmv["ms_per_term"], "non_term_ms_per_step": non_term_ms,
+                "ms_per_term": spmv["ms_per_term"], "ms_per_term_in_series": ms_term_series,
+                "non_term_ms_per_step": non_term_ms,
                 "breakdown_ms_per_step": breakdown, "setup_s": setup_s, "spmv": spmv,
                 "stage2": stage2, "pcg": pcg}
         print(json.dumps(line), flush=True)
