@@ -1375,7 +1375,10 @@ static void op_power(pv_ctx* c, int max_order, double thr, int* order, double* t
   c->check_launch();
   CK(cudaEventRecord(c->tev[1], c->stream));
   int launched_terms = 0;
-  if (series || (c->tune.graph && !c->loop && max_order > 0)) {  // the device-driven term loop
+  // the device-driven term loop: single-rank contexts (with world > 1 the host look-ahead
+  // loop below drives the terms, an NCCL call between kernels: a multi-rank collective inside
+  // a conditional graph body has never been executed on this 1-GPU pool)
+  if (series || (c->tune.graph && !c->loop && c->world == 1 && max_order > 0)) {
     long long body_launches = 0;
     if (series) {
       launch_series<S>(c, max_order, thr);
