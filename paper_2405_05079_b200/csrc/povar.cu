@@ -171,6 +171,7 @@ struct pv_ctx {
   int64_t solve_us[3] = {0, 0, 0};  // last power solve: RHS, terms, back-substitution
   int64_t solve_terms_launched = 0;
   TermGraph tgraph;
+  TermGraph bsgraph;  // the blocked back-substitution as one captured graph (same validity key)
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
@@ -1334,7 +1335,45 @@ static void mark_rhs(pv_ctx* c) {
 // v = x (the pose update in cx), block by block so that each block's s stays in L2
 // (back_substitute, normal_eq.py:239-250)
 template <int S>
+static void back_substitute_launches(pv_ctx* c);
+
+// The 2 B + 1 launches of the back-substitution replayed as one CUDA graph (single-rank
+// contexts, PV_OPT_GRAPH): no control flow, only the launch gaps of a stream are saved.
+template <int S>
 static void back_substitute_dev(pv_ctx* c) {
+  if (!(c->tune.graph && !c->loop && c->world == 1)) {
+    back_substitute_launches<S>(c);
+    return;
+  }
+  TermGraph& G = c->bsgraph;
+  const int xm = c->xm_ok ? 1 : 0;
+  if (!(G.exec && G.stage == S && G.n_blk == c->n_blk && G.wpc == c->wpc && G.xm == xm &&
+        G.coll == c->collective() && G.layout_gen == c->layout_gen &&
+        std::memcmp(&G.tune, &c->tune, sizeof(Tune)) == 0)) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    G = TermGraph{};
+    const long long l0 = c->launches;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    back_substitute_launches<S>(c);
+    CK(cudaStreamEndCapture(c->stream, &G.graph));
+    G.body_launches = c->launches - l0;
+    c->launches = l0;
+    CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+    G.stage = S;
+    G.n_blk = c->n_blk;
+    G.wpc = c->wpc;
+    G.xm = xm;
+    G.layout_gen = c->layout_gen;
+    G.tune = c->tune;
+    G.coll = c->collective();
+  }
+  CK(cudaGraphLaunch(G.exec, c->stream));
+  c->launches += G.body_launches;
+}
+
+template <int S>
+static void back_substitute_launches(pv_ctx* c) {
   k_setv<S><<<blocks_for(c->n_p, 128), 128, 0, c->stream>>>((int)c->n_p, c->cx, c->ch, c->crec);
   c->launched();
   for (int b = 0; b < c->n_blk; ++b) {
@@ -1742,6 +1781,8 @@ void pv_destroy(pv_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->tgraph.exec) cudaGraphExecDestroy(c->tgraph.exec);
   if (c->tgraph.graph) cudaGraphDestroy(c->tgraph.graph);
+  if (c->bsgraph.exec) cudaGraphExecDestroy(c->bsgraph.exec);
+  if (c->bsgraph.graph) cudaGraphDestroy(c->bsgraph.graph);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
