@@ -172,6 +172,7 @@ struct pv_ctx {
   int64_t solve_terms_launched = 0;
   TermGraph tgraph;
   TermGraph bsgraph;  // the blocked back-substitution as one captured graph (same validity key)
+  TermGraph pcggraph; // one PCG iteration (blocked S'.p + the three vector kernels), thr = tolerance
   int4* d_items = nullptr;
   int* d_item_off = nullptr;
   size_t items_bytes = 0, item_off_bytes = 0;
@@ -1534,7 +1535,9 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
   // iterations with a one-iteration look-ahead on the device stop flag; as in op_power the
   // host acts only on a stop taken at an iteration known complete (rank-consistent)
   const bool stopped0 = ((volatile PowerCtl*)c->host_ctl)->stopped != 0;  // after the sync
-  for (int it = 1; it <= max_it && !stopped0; ++it) {
+  // one iteration: the blocked S'.p (the term kernels, launched ahead of the stop flag) and the
+  // three vector kernels; `it` < 0: the iteration count is kept on the device
+  auto launch_iteration = [&](int it) {
     launch_cam<S, false, EP_NONE, true>(c, cam_args(0, 0, 0, 0, 1, 0, 0.0, 1));
     for (int b = 0; b < B; ++b) {
       launch_lm_reduce<S, LR_TERM>(c, b, b + 1, 1);
@@ -1550,6 +1553,44 @@ static void op_pcg(pv_ctx* c, int max_it, double tol, int* its, double* rel, int
                                                c->host_ctl_dev, c->ticket);
     k_pcg_dir<S><<<wg, 256, 0, c->stream>>>((int)np, c->ch, c->crec, v, c->ctl);
     c->launched(3);
+  };
+  // single-rank contexts replay the iteration as a captured graph (PV_OPT_GRAPH): the same
+  // kernels without a stream's launch gaps; the host look-ahead loop stays
+  TermGraph* PG = nullptr;
+  if (c->tune.graph && !c->loop && c->world == 1 && !stopped0 && max_it > 0) {
+    TermGraph& G = c->pcggraph;
+    const int xm = c->xm_ok ? 1 : 0;
+    if (!(G.exec && G.stage == S && G.thr == tol && G.n_blk == c->n_blk && G.wpc == c->wpc &&
+          G.xm == xm && G.coll == c->collective() && G.layout_gen == c->layout_gen &&
+          std::memcmp(&G.tune, &c->tune, sizeof(Tune)) == 0)) {
+      if (G.exec) cudaGraphExecDestroy(G.exec);
+      if (G.graph) cudaGraphDestroy(G.graph);
+      G = TermGraph{};
+      const long long l0 = c->launches;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+      launch_iteration(-1);
+      CK(cudaStreamEndCapture(c->stream, &G.graph));
+      G.body_launches = c->launches - l0;
+      c->launches = l0;
+      CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+      G.stage = S;
+      G.thr = tol;
+      G.n_blk = c->n_blk;
+      G.wpc = c->wpc;
+      G.xm = xm;
+      G.layout_gen = c->layout_gen;
+      G.tune = c->tune;
+      G.coll = c->collective();
+    }
+    PG = &G;
+  }
+  for (int it = 1; it <= max_it && !stopped0; ++it) {
+    if (PG) {
+      CK(cudaGraphLaunch(PG->exec, c->stream));
+      c->launches += PG->body_launches;
+    } else {
+      launch_iteration(it);
+    }
     CK(cudaEventRecord(c->ev[it & 1], c->stream));
     if (it >= 2) {
       CK(cudaEventSynchronize(c->ev[(it - 1) & 1]));
@@ -1783,6 +1824,8 @@ void pv_destroy(pv_ctx* c) {
   if (c->tgraph.graph) cudaGraphDestroy(c->tgraph.graph);
   if (c->bsgraph.exec) cudaGraphExecDestroy(c->bsgraph.exec);
   if (c->bsgraph.graph) cudaGraphDestroy(c->bsgraph.graph);
+  if (c->pcggraph.exec) cudaGraphExecDestroy(c->pcggraph.exec);
+  if (c->pcggraph.graph) cudaGraphDestroy(c->pcggraph.graph);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;

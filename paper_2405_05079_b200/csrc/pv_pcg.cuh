@@ -423,7 +423,8 @@ __global__ void k_pcg_curv(int n_p, int it, const double* __restrict__ cy,
   double tot[1];
   if (!last_cta_sum<1>(part, n_p, ticket, tot) || threadIdx.x != 0) return;
   PowerCtl c = *ctl;
-  c.order = it;  // iterations = it (solvers.py:174)
+  c.order = it >= 0 ? it : c.order + 1;  // iterations = it (solvers.py:174); -1: count here
+                                          // (the iteration replayed as a captured graph)
   if (tot[0] <= 0.0) {  // solvers.py:177-179
     c.stopped = 1;
     c.pad = 1;  // "breakdown"
